@@ -1,0 +1,40 @@
+// cham_pool.h — internal definition of the paged adapter pool (not part of the C ABI).
+#pragma once
+
+#include <vector>
+
+#include "cham_common.cuh"
+
+struct cham_pool {
+  int device = 0;
+  int n_pages = 0;
+  int n_layers = 0;
+  int n_proj = 0;
+  int dtype = CHAM_BF16;
+  int es = 2;  // element bytes
+  int n_slots = 0;
+  int max_tokens = 0;
+  int sm_count = 148;
+  std::vector<int> h_in, h_out;
+  std::vector<size_t> a_off, b_off;  // byte offset of (l*n_proj+p) A / B block inside a page
+  size_t page_bytes = 0;
+  char* base = nullptr;                // n_pages * page_bytes, device
+  int* d_slot_pages = nullptr;         // [n_slots][kMaxPagesPerSlot]
+  int* d_slot_rank = nullptr;          // [n_slots]
+  std::vector<int> slot_rank;          // host mirror
+  std::vector<int> slot_pages;         // host mirror [n_slots][kMaxPagesPerSlot]
+  // decode / shrink / expand workspace (one launch at a time per pool)
+  int* d_ctr = nullptr;                // [0] item counter, [1] finished CTAs
+  int* d_tile_done = nullptr;          // [kMaxJobs * max_tokens]
+  float* d_vws = nullptr;              // [kMaxJobs][max_tokens][vws_kc][kMaxRank]
+  int vws_kc = 1;
+};
+
+namespace cham {
+// Byte offset of element (row j, element e) inside a 1 KiB swizzled atom.
+__host__ __device__ inline uint32_t atom_offset(int j, int e, int es) {
+  const int byte = e * es;
+  const int chunk = byte >> 4;
+  return static_cast<uint32_t>(j * kRowBytes + (((chunk ^ j) & 7) << 4) + (byte & 15));
+}
+}  // namespace cham

@@ -1,0 +1,198 @@
+"""GPU parity: the fused decode kernel (K1+K2) through the C ABI vs the numpy oracle.
+
+Tolerances (BASELINE.json north_star): fp32 rtol 1e-5; bf16 with fp32 accumulation rtol 2e-2
+against the oracle run on the same bf16-rounded inputs.  A non-zero base y0 keeps relative
+errors well-posed; the absolute floor is stated per test.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.lora_ref import bf16_round, lora_apply_ref, lora_expand_ref, lora_shrink_ref, make_adapters
+from oracle.segments_ref import build_segments_ref
+
+pytestmark = pytest.mark.gpu
+
+FP32_RTOL, FP32_ATOL = 1e-5, 1e-5
+BF16_RTOL, BF16_ATOL = 2e-2, 2e-2
+
+
+def _pool(n_layers, h_in, h_out, dtype, n_pages, n_slots=64, max_tokens=4096):
+    from paper_2411_17741_b200.pool import AdapterPool
+
+    return AdapterPool(n_pages, n_layers, h_in, h_out, dtype=dtype, n_slots=n_slots, max_tokens=max_tokens)
+
+
+def _install(pool, adapters_lp, slot_ranks, device_pack=False):
+    """adapters_lp: slot -> list over (l,p) of (A, B) numpy arrays.  Binds pages in order."""
+    next_page = 0
+    for slot, r in slot_ranks.items():
+        npg = -(-r // 8)
+        pages = list(range(next_page, next_page + npg))
+        next_page += npg
+        pool.set_slot(slot, r, pages)
+        a_list = [torch.from_numpy(a) for a, _ in adapters_lp[slot]]
+        b_list = [torch.from_numpy(b) for _, b in adapters_lp[slot]]
+        if device_pack:
+            packed = pool.pack_device(a_list, b_list, r)
+            pool.fill_from_device(slot, packed)
+        else:
+            packed = pool.pack_host(a_list, b_list, r)
+            pool.fill_async(slot, packed)
+    torch.cuda.synchronize()
+
+
+def _run_case(dtype, h_in, h_out, slot_ranks, req_slots, req_ntok, seed=0, device_pack=False, perm_identity=False):
+    rng = np.random.default_rng(seed)
+    bf16 = dtype == torch.bfloat16
+    adapters = make_adapters(rng, slot_ranks, h_in, h_out, bf16=bf16)
+    T = int(np.sum(req_ntok))
+    x = rng.standard_normal((T, h_in)).astype(np.float32)
+    y0 = rng.standard_normal((T, h_out)).astype(np.float32)
+    if bf16:
+        x, y0 = bf16_round(x), bf16_round(y0)
+    npages = sum(-(-r // 8) for r in slot_ranks.values())
+    pool = _pool(1, [h_in], [h_out], dtype, npages)
+    _install(pool, {s: [adapters[s]] for s in slot_ranks}, slot_ranks, device_pack=device_pack)
+    req_rank = [slot_ranks[s] if s >= 0 else 0 for s in req_slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(req_slots, req_rank, req_ntok)
+    from paper_2411_17741_b200.ops import lora_apply
+
+    xd = torch.from_numpy(x).to("cuda", dtype)
+    yd = torch.from_numpy(y0).to("cuda", dtype)
+    lora_apply(xd, yd, seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=0,
+               perm=None if perm_identity else perm)
+    torch.cuda.synchronize()
+    got = yd.float().cpu().numpy()
+    ref = lora_apply_ref(x, y0, None if perm_identity else perm, seg_off, seg_slot, seg_rank, adapters)
+    pool.close()
+    return got, ref
+
+
+def _c1_batch():
+    # 4 adapters ranks [8, 8, 16, 16], 32 requests, rng(0).integers(0, 4, 32)
+    slots = np.random.default_rng(0).integers(0, 4, 32).tolist()
+    return {0: 8, 1: 8, 2: 16, 3: 16}, slots
+
+
+def test_c1_fp32_decode_rtol_1e5():
+    slot_ranks, slots = _c1_batch()
+    got, ref = _run_case(torch.float32, 4096, 4096, slot_ranks, slots, [1] * 32)
+    np.testing.assert_allclose(got, ref, rtol=FP32_RTOL, atol=FP32_ATOL)
+
+
+def test_c1_fp32_device_pack_matches_host_pack():
+    slot_ranks, slots = _c1_batch()
+    got, ref = _run_case(torch.float32, 4096, 4096, slot_ranks, slots, [1] * 32, device_pack=True)
+    np.testing.assert_allclose(got, ref, rtol=FP32_RTOL, atol=FP32_ATOL)
+
+
+@pytest.mark.parametrize("ranks", [(8, 16, 32, 64, 128), (24, 40, 128, 256)])
+def test_bf16_mixed_ranks(ranks):
+    rng = np.random.default_rng(1)
+    slot_ranks = {i: r for i, r in enumerate(ranks)}
+    slots = rng.integers(0, len(ranks), 96).tolist()
+    got, ref = _run_case(torch.bfloat16, 4096, 4096, slot_ranks, slots, [1] * 96, seed=1)
+    np.testing.assert_allclose(got, bf16_round(ref.astype(np.float32)), rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_bf16_multitoken_segments_and_no_adapter_rows():
+    # prefill-like requests (several tokens) and requests without an adapter (slot -1)
+    slot_ranks = {3: 16, 7: 64, 9: 8}
+    slots = [3, -1, 7, 9, 3, 7, -1, 9]
+    ntok = [5, 3, 9, 1, 2, 7, 4, 13]
+    got, ref = _run_case(torch.bfloat16, 4096, 4096, slot_ranks, slots, ntok, seed=2)
+    np.testing.assert_allclose(got, bf16_round(ref.astype(np.float32)), rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_bf16_gqa_shapes_70b_kv():
+    # Llama-2-70B k/v projection: 8192 -> 1024 (C5 dims), rank 64
+    slot_ranks = {0: 64, 1: 32}
+    slots = [0, 1] * 20
+    got, ref = _run_case(torch.bfloat16, 8192, 1024, slot_ranks, slots, [1] * 40, seed=3)
+    np.testing.assert_allclose(got, bf16_round(ref.astype(np.float32)), rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_fp32_rectangular_and_identity_perm():
+    slot_ranks = {0: 16}
+    got, ref = _run_case(torch.float32, 2048, 1024, slot_ranks, [0] * 7, [1] * 7, seed=4, perm_identity=True)
+    np.testing.assert_allclose(got, ref, rtol=FP32_RTOL, atol=FP32_ATOL)
+
+
+def test_empty_batch_is_noop():
+    from paper_2411_17741_b200.ops import lora_apply
+
+    pool = _pool(1, [4096], [4096], torch.bfloat16, 1)
+    x = torch.zeros(0, 4096, dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros(0, 4096, dtype=torch.bfloat16, device="cuda")
+    lora_apply(x, y, [], [0], [], pool=pool, layer=0, proj=0)
+    torch.cuda.synchronize()
+    pool.close()
+
+
+def test_repeated_launches_reset_workspace():
+    """The persistent kernel resets its counters itself: back-to-back launches stay exact."""
+    slot_ranks, slots = _c1_batch()
+    rng = np.random.default_rng(5)
+    adapters = make_adapters(rng, slot_ranks, 4096, 4096)
+    x = rng.standard_normal((32, 4096)).astype(np.float32)
+    y0 = rng.standard_normal((32, 4096)).astype(np.float32)
+    pool = _pool(1, [4096], [4096], torch.float32, 6)
+    _install(pool, {s: [adapters[s]] for s in slot_ranks}, slot_ranks)
+    req_rank = [slot_ranks[s] for s in slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(slots, req_rank, [1] * 32)
+    from paper_2411_17741_b200.ops import lora_apply
+
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.from_numpy(y0).cuda()
+    for _ in range(5):
+        lora_apply(xd, yd, seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=0, perm=perm)
+    torch.cuda.synchronize()
+    ref = y0.astype(np.float64)
+    for _ in range(5):
+        ref = lora_apply_ref(x, ref, perm, seg_off, seg_slot, seg_rank, adapters)
+    np.testing.assert_allclose(yd.cpu().numpy(), ref, rtol=1e-5, atol=5e-5)
+    pool.close()
+
+
+def test_shrink_expand_halves_match_fused():
+    slot_ranks = {0: 8, 1: 64, 2: 128}
+    rng = np.random.default_rng(6)
+    slots = rng.integers(0, 3, 40).tolist()
+    adapters = make_adapters(rng, slot_ranks, 4096, 4096)
+    x = rng.standard_normal((40, 4096)).astype(np.float32)
+    y0 = rng.standard_normal((40, 4096)).astype(np.float32)
+    pool = _pool(1, [4096], [4096], torch.float32, 25)
+    _install(pool, {s: [adapters[s]] for s in slot_ranks}, slot_ranks)
+    req_rank = [slot_ranks[s] for s in slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(slots, req_rank, [1] * 40)
+    from paper_2411_17741_b200.ops import lora_expand, lora_shrink
+
+    xd = torch.from_numpy(x).cuda()
+    v = torch.zeros(40, 128, dtype=torch.float32, device="cuda")
+    lora_shrink(xd, v, seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=0, perm=perm)
+    torch.cuda.synchronize()
+    v_ref = lora_shrink_ref(x, perm, seg_off, seg_slot, seg_rank, adapters, 128)
+    np.testing.assert_allclose(v.cpu().numpy(), v_ref, rtol=1e-5, atol=1e-5)
+    yd = torch.from_numpy(y0).cuda()
+    lora_expand(v, yd, seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=0, perm=perm)
+    torch.cuda.synchronize()
+    ref = lora_expand_ref(v_ref, y0, perm, seg_off, seg_slot, seg_rank, adapters)
+    np.testing.assert_allclose(yd.cpu().numpy(), ref, rtol=1e-5, atol=1e-5)
+    pool.close()
+
+
+def test_device_segment_builder_bit_exact():
+    from paper_2411_17741_b200.ops import build_segments
+
+    rng = np.random.default_rng(7)
+    for n_req, n_slots in [(1, 1), (256, 82), (4096, 1000), (333, 7), (64, 64)]:
+        slots = rng.integers(-1, n_slots, n_req)
+        ranks = rng.choice([8, 16, 32, 64, 128], n_req)
+        ntok = rng.integers(1, 6, n_req)
+        tbl = build_segments(slots, ranks, ntok)
+        torch.cuda.synchronize()
+        got = tbl.to_host()
+        want = build_segments_ref(slots, ranks, ntok)
+        for g, w in zip(got, want):
+            np.testing.assert_array_equal(g, w)
