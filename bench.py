@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: batched heterogeneous-rank LoRA apply on B200 (BASELINE.json metric).
+
+Workload (N=1 line): BASELINE config C2 — Llama-2-7B dims (h=4096, 32 layers, q/k/v/o all
+4096->4096), 100-adapter catalog (20 per rank in {8,16,32,64,128}), one decode batch of
+256 tokens with adapters drawn by the reference's assign_adapter(default_rng(seed)).
+A step = the device segment-table build (K4) + LoRA apply for all 32 layers x 4 projections
+(q/k/v fused into one launch over their shared input, o separate), replayed as one CUDA graph.
+Synthetic random-init adapters (pool pages filled with N(0, 0.02) bf16) and activations.
+
+value    = tokens/s over all ranks, inputs resident in HBM (max over ranks of the CUDA-event time)
+e2e      = tokens/s through LoraStepExecutor with host buffers: pinned H2D of the request
+           table + the step's hidden state, the step's graph, D2H of the last projection's output
+roofline = algorithmic bytes of the apply launches / their measured duration vs
+           MEASURED_PEAKS.json hbm_gbs
+cpu_baseline = the numpy oracle (oracle/lora_ref.py) on the host cores, bounded sample
+--impl reference = that CPU path alone, on the same config/metric (the reference has no CPU
+           LoRA implementation of its own — it only models the cost, engine.py:67-77).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LoRA-apply tokens/sec and adapter-read HBM GB/s (% of peak), mixed ranks, 1/2/4/8 GPU"
+H = 4096
+N_LAYERS = 32
+N_PROJ = 4
+T_DECODE = 256
+NUM_ADAPTERS = 100
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1681.7)), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def algorithmic_bytes(seg_off, seg_slot, seg_rank, n_tokens, h_in, h_out, es):
+    """SURVEY §8(d) per (layer, proj): every distinct adapter once (A and B) plus
+    T * (h_in reads of x + h_out reads and writes of y)."""
+    distinct = {}
+    for i in range(len(seg_slot)):
+        if seg_slot[i] >= 0 and seg_off[i + 1] > seg_off[i]:
+            distinct[int(seg_slot[i])] = int(seg_rank[i])
+    adapter = sum(r * (h_in + h_out) * es for r in distinct.values())
+    act = n_tokens * (h_in + 2 * h_out) * es
+    return adapter, act
+
+
+# --------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- CPU path
+def cpu_oracle_sample(batch_ids, seconds: float = 12.0):
+    """numpy fp32 restatement (oracle/lora_ref.py) of one (layer, proj) apply of the batch,
+    repeated for ~`seconds`; returns (seconds per layer-proj, cores, sample description)."""
+    from oracle.lora_ref import lora_apply_ref
+    from oracle.segments_ref import build_segments_ref
+    from paper_2411_17741_b200.workload import rank_of_id
+
+    rng = np.random.default_rng(0)
+    uniq = sorted(set(batch_ids))
+    slot = {a: i for i, a in enumerate(uniq)}
+    adapters = {}
+    for a in uniq:
+        r = rank_of_id(a)
+        adapters[slot[a]] = ((rng.standard_normal((H, r)) * 0.02).astype(np.float32),
+                             (rng.standard_normal((r, H)) * 0.02).astype(np.float32))
+    ranks = [rank_of_id(a) for a in batch_ids]
+    slots = [slot[a] for a in batch_ids]
+    perm, off, sl, rk = build_segments_ref(slots, ranks, [1] * len(batch_ids))
+    x = rng.standard_normal((len(batch_ids), H)).astype(np.float32)
+    y = rng.standard_normal((len(batch_ids), H)).astype(np.float32)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        lora_apply_ref(x, y, perm, off, sl, rk, adapters, acc=np.float32)
+        n += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = (time.perf_counter() - t0) / n
+    cores = len(os.sched_getaffinity(0))
+    return dt, cores, f"{n} x one (layer,proj) apply of the C2 batch ({len(batch_ids)} tok, {len(uniq)} adapters), numpy fp32"
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    from paper_2411_17741_b200.workload import decode_batch
+
+    batch = decode_batch(0, T_DECODE, NUM_ADAPTERS)
+    per_step = []
+    t_lp = None
+    for _ in range(args.warmup):
+        t_lp, cores, sample = cpu_oracle_sample(batch, seconds=0.5)
+    for _ in range(args.steps):
+        t_lp, cores, sample = cpu_oracle_sample(batch, seconds=max(1.0, 20.0 / max(args.steps, 1)))
+        per_step.append(t_lp * N_LAYERS * N_PROJ)
+    step_s = statistics.median(per_step)
+    value = T_DECODE / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: Llama-2-7B q/k/v/o LoRA, 100 adapters ranks 8-128, decode batch 256 tokens",
+                   "global_batch": T_DECODE, "seq_len": 1, "parallelism": "replicas", "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": sample + f"; step = 128 x that, per-step time = median of {args.steps}"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU path
+def run_ours(args, rank: int, world: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_17741_b200.executor import LoraStepExecutor
+    from paper_2411_17741_b200.model import build_catalog
+    from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
+    from paper_2411_17741_b200.workload import decode_batch, rank_of_id
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    catalog = build_catalog(NUM_ADAPTERS)
+    ids = list(catalog)
+    slot_of = {a: i for i, a in enumerate(ids)}
+    n_pages = sum(pages_for_rank(s.rank) for s in catalog.values())
+    pool = AdapterPool(n_pages, N_LAYERS, [H] * N_PROJ, [H] * N_PROJ, dtype=torch.bfloat16,
+                       n_slots=len(ids), max_tokens=4096, device=dev)
+    # synthetic random-init adapters: every page of every adapter gets N(0, 0.02) bf16 values
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    page = 0
+    for a in ids:
+        r = catalog[a].rank
+        npg = pages_for_rank(r)
+        pool.set_slot(slot_of[a], r, list(range(page, page + npg)))
+        buf = (torch.randn(npg * pool.page_bytes // 2, generator=gen, device=dev) * 0.02).to(torch.bfloat16)
+        pool.fill_from_device(slot_of[a], buf.view(torch.uint8))
+        page += npg
+        del buf
+    torch.cuda.synchronize(dev)
+
+    batch = decode_batch(rank, T_DECODE, NUM_ADAPTERS)
+    req_slot = np.array([slot_of[a] for a in batch], dtype=np.int32)
+    req_rank = np.array([rank_of_id(a) for a in batch], dtype=np.int32)
+    req_ntok = np.ones(len(batch), dtype=np.int32)
+
+    groups = [[0, 1, 2], [3]] if args.mode == "qkv" else [[0], [1], [2], [3]]
+    ex = LoraStepExecutor(pool, max_requests=1024, max_tokens=4096, proj_groups=groups)
+    T = int(req_ntok.sum())
+    xs = [[torch.randn(T, H, device=dev).to(torch.bfloat16) for _ in groups] for _ in range(N_LAYERS)]
+    ys = [[torch.randn(T, H, device=dev).to(torch.bfloat16) for _ in range(N_PROJ)] for _ in range(N_LAYERS)]
+    ex.upload(req_slot, req_rank, req_ntok)
+    torch.cuda.synchronize(dev)
+
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        ex.run(xs, ys)  # eager warm-up (sets kernel attributes before capture)
+    torch.cuda.synchronize(dev)
+    g_step = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_step, stream=s):
+        ex.run(xs, ys)
+    g_apply = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_apply, stream=s):
+        for layer in range(N_LAYERS):
+            ex.apply_layer(layer, xs[layer], ys[layer])
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- timed region: K step replays, inputs resident in HBM
+    with torch.cuda.stream(s):
+        for _ in range(args.warmup):
+            g_step.replay()
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        with torch.cuda.stream(s):
+            ev0.record(s)
+            for _ in range(args.steps):
+                g_step.replay()
+            ev1.record(s)
+        torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        step_ms = ev0.elapsed_time(ev1) / args.steps
+        # apply-only graph for the roofline (the decode kernel launches alone)
+        reps = max(3, args.steps)
+        with torch.cuda.stream(s):
+            ev0.record(s)
+            for _ in range(reps):
+                g_apply.replay()
+            ev1.record(s)
+        torch.cuda.synchronize(dev)
+        apply_ms = ev0.elapsed_time(ev1) / reps
+    step_ms = max_over_ranks(step_ms)
+    apply_ms_max = max_over_ranks(apply_ms)
+
+    # ---- e2e: through the executor with host buffers (pinned H2D request table + hidden
+    #      state, step graph, D2H of the last projection's output), wall clock per step
+    x_host = torch.randn(T, H).to(torch.bfloat16).pin_memory()
+    y_host = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+    h2d = 3 * len(batch) * 4 + x_host.numel() * 2
+    d2h = y_host.numel() * 2
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s):
+            ex.upload(req_slot, req_rank, req_ntok, stream=s)
+            xs[0][0].copy_(x_host, non_blocking=True)
+            g_step.replay()
+            y_host.copy_(ys[N_LAYERS - 1][N_PROJ - 1], non_blocking=True)
+        s.synchronize()
+        if i >= args.warmup:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(statistics.median(e2e_times))
+
+    # ---- algorithmic bytes / flops from the rank's segment table
+    perm, off, sl, rk = ex.table.to_host()
+    a_bytes, act_bytes = algorithmic_bytes(off, sl, rk, T, H, H, 2)
+    a_bytes, act_bytes = int(a_bytes), int(act_bytes)
+    lp = N_LAYERS * N_PROJ
+    bytes_step = (a_bytes + act_bytes) * lp
+    adapter_bytes_step = a_bytes * lp
+    flops_step = int(2 * sum(int(rk[i]) * int(off[i + 1] - off[i]) for i in range(len(sl))) * (H + H) * lp)
+    hbm_peak, _, peak_kind = peaks()
+    apply_launches = N_LAYERS * len(groups)
+    achieved = bytes_step / (apply_ms * 1e-3) / 1e9
+
+    if rank == 0:
+        tokens_total = T * world
+        value = tokens_total / (step_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "C2: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers), 100 adapters ranks 8-128, "
+                                   "decode batch 256 tokens per GPU (assign_adapter seed = rank)",
+                       "global_batch": tokens_total, "seq_len": 1, "parallelism": f"replicas x{world}",
+                       "launch_mode": args.mode,
+                       "l2": "inputs larger than L2: each step streams 8 GB of distinct adapter pages "
+                             "(128 (layer,proj) blocks) through the 126 MB L2"},
+            "adapter_read_gbs": adapter_bytes_step / (step_ms * 1e-3) / 1e9,
+            "adapter_read_frac_of_peak": adapter_bytes_step / (step_ms * 1e-3) / 1e9 / hbm_peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                         "kernel": "lora_decode_kernel<bf16> (fused shrink->expand)",
+                         "bytes_per_step": bytes_step, "launches_per_step": apply_launches,
+                         "avg_launch_us": apply_ms * 1e3 / apply_launches,
+                         "traffic": None},
+            "flops_per_step": flops_step,
+            "e2e": {"value": tokens_total / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": args.steps * ex.launches_per_step(),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            t_lp, cores, sample = cpu_oracle_sample(batch, seconds=args.cpu_seconds)
+            line["cpu_baseline"] = {"value": T / (t_lp * lp), "unit": "tokens/s", "cores": cores, "kind": "port",
+                                    "sample": sample + "; tokens/s = 256 / (128 x that)"}
+        print(json.dumps(line), flush=True)
+    pool.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["qkv", "per-proj"], default="qkv")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        dist.init_process_group(backend=backend)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -28,7 +28,7 @@ constexpr int kAtomBytes = 1024;       // 8 rows x 128 B swizzle atom
 constexpr int kRowBytes = 128;
 constexpr int kMaxRank = 256;          // RMAX: v workspace row stride
 constexpr int kMaxPagesPerSlot = kMaxRank / kRowsPerPage;
-constexpr int kMaxSegments = 1024;
+constexpr int kMaxSegments = 512;
 constexpr int kMaxJobs = 4;
 constexpr int kMaxRequests = 4096;
 constexpr int kActRowBytes = 4096;     // activation bytes per token per decode item (k-chunk)

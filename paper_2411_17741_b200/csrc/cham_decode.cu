@@ -40,7 +40,10 @@ constexpr int NGROUP = 2;
 constexpr int GROUP_WARPS = 4;
 constexpr int GROUP_THREADS = GROUP_WARPS * 32;
 constexpr int NTHREADS = 32 + NGROUP * GROUP_THREADS;
-constexpr int PLAN_SEGS = 1024;             // segments cached in shared memory
+constexpr int PLAN_SEGS = 512;              // segments per launch (plan lives in shared memory)
+constexpr int PLAN_PAGES = 2048;            // page ids cached in shared memory (else read from L2)
+constexpr int PLAN_TOKENS = 2048;           // perm entries cached in shared memory (else from L2)
+static_assert(PLAN_SEGS == kMaxSegments, "limits");
 
 enum Mode { MODE_FUSED = 0, MODE_SHRINK = 1, MODE_EXPAND = 2 };
 enum Kind { KIND_END = 0, KIND_SHRINK = 1, KIND_EXPAND = 2 };
@@ -74,7 +77,15 @@ struct Params {
   float* v_out;       // MODE_SHRINK
   const float* v_in;  // MODE_EXPAND
   int v_stride;
+  unsigned long long* trace;  // debug: [cta][seq][4] globaltimer stamps (null = off)
+  int trace_cap;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Meta {
   int kind, job, pos0, T, g, kc, np, col0, ncols, nq, p2, need;
@@ -89,12 +100,15 @@ struct Shared {
   int sh_start[PLAN_SEGS + 1];
   int ex_start[PLAN_SEGS + 1];
   int seg_off[PLAN_SEGS + 1];
-  int seg_sr[PLAN_SEGS];  // (slot << 9) | rank, slot -1 -> 0 rank
+  int seg_pg[PLAN_SEGS + 1];  // prefix of pages per segment into `pages`
+  int seg_sr[PLAN_SEGS];      // (slot << 9) | rank, slot -1 -> 0 rank
+  uint16_t pages[PLAN_PAGES];
+  uint16_t perm[PLAN_TOKENS];
   float red[NGROUP][GROUP_WARPS][32];
   float vs[NGROUP][TG][kMaxRank];
-  int scan[NTHREADS / 32][2];
+  int scan[NTHREADS / 32][3];
   int flag[NGROUP];
-  int totals[3];  // total shrink items/job, total expand items/job, total tokens
+  int totals[4];  // shrink items/job, expand items/job, tokens, pages
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -160,7 +174,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
   {
     const int per = ceil_div(S, NTHREADS);
     const int s0 = min(S, tid * per), s1 = min(S, s0 + per);
-    int lsh = 0, lex = 0;
+    int lsh = 0, lex = 0, lpg = 0;
     for (int s = s0; s < s1; ++s) {
       const int o0 = p.seg_off[s], o1 = p.seg_off[s + 1];
       const int slot = p.seg_slot[s];
@@ -171,41 +185,64 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
       plan_counts<T>(p, o1 - o0, rank, a, b);
       lsh += a;
       lex += b;
+      lpg += ceil_div(rank, kRowsPerPage);
     }
-    // block exclusive scan of (lsh, lex)
-    int ish = lsh, iex = lex;
+    // block exclusive scan of (lsh, lex, lpg)
+    int ish = lsh, iex = lex, ipg = lpg;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int a = __shfl_up_sync(0xffffffffu, ish, o);
-      int b = __shfl_up_sync(0xffffffffu, iex, o);
-      if (lane >= o) { ish += a; iex += b; }
+      const int a = __shfl_up_sync(0xffffffffu, ish, o);
+      const int b = __shfl_up_sync(0xffffffffu, iex, o);
+      const int c = __shfl_up_sync(0xffffffffu, ipg, o);
+      if (lane >= o) { ish += a; iex += b; ipg += c; }
     }
-    if (lane == 31) { sm.scan[warp][0] = ish; sm.scan[warp][1] = iex; }
+    if (lane == 31) { sm.scan[warp][0] = ish; sm.scan[warp][1] = iex; sm.scan[warp][2] = ipg; }
     __syncthreads();
-    int bsh = 0, bex = 0;
-    for (int w = 0; w < warp; ++w) { bsh += sm.scan[w][0]; bex += sm.scan[w][1]; }
+    int bsh = 0, bex = 0, bpg = 0;
+    for (int w = 0; w < warp; ++w) { bsh += sm.scan[w][0]; bex += sm.scan[w][1]; bpg += sm.scan[w][2]; }
     bsh += ish - lsh;
     bex += iex - lex;
+    bpg += ipg - lpg;
     for (int s = s0; s < s1; ++s) {
       const int rank = sm.seg_sr[s] & 511;
       int a, b;
       plan_counts<T>(p, p.seg_off[s + 1] - sm.seg_off[s], rank, a, b);
       sm.sh_start[s] = bsh;
       sm.ex_start[s] = bex;
+      sm.seg_pg[s] = bpg;
       bsh += a;
       bex += b;
+      bpg += ceil_div(rank, kRowsPerPage);
     }
     if (tid == NTHREADS - 1) {
       sm.sh_start[S] = bsh;
       sm.ex_start[S] = bex;
+      sm.seg_pg[S] = bpg;
       sm.seg_off[S] = S > 0 ? p.seg_off[S] : 0;
       sm.totals[0] = bsh;
       sm.totals[1] = bex;
       sm.totals[2] = S > 0 ? p.seg_off[S] : 0;
+      sm.totals[3] = bpg;
+    }
+    __syncthreads();
+    // page ids and perm into shared memory when they fit (the producer then never waits on L2)
+    if (sm.totals[3] <= PLAN_PAGES) {
+      for (int s = s0; s < s1; ++s) {
+        const int slot = sm.seg_sr[s] >> 9;
+        const int np = ceil_div(sm.seg_sr[s] & 511, kRowsPerPage);
+        for (int g = 0; g < np; ++g)
+          sm.pages[sm.seg_pg[s] + g] = (uint16_t)__ldg(p.slot_pages + slot * kMaxPagesPerSlot + g);
+      }
+    }
+    if (sm.totals[2] <= PLAN_TOKENS) {
+      for (int i = tid; i < sm.totals[2]; i += NTHREADS)
+        sm.perm[i] = (uint16_t)(p.perm ? __ldg(p.perm + i) : i);
     }
     __syncthreads();
   }
   const int SH = sm.totals[0], EX = sm.totals[1], NTOK = sm.totals[2];
+  const bool pages_smem = sm.totals[3] <= PLAN_PAGES;
+  const bool perm_smem = NTOK <= PLAN_TOKENS;
   if (NTOK > p.max_tokens) {
     if (tid == 0 && blockIdx.x == 0) p.ctr[2] = CHAM_ERR_LIMIT;
     return;
@@ -272,14 +309,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
       }
       const int pos0 = o0 + tile * TG;
       const int tcount = min(TG, Ts - tile * TG);
-      int row = 0;
-      if (lane < tcount) row = p.perm ? __ldg(p.perm + pos0 + lane) : pos0 + lane;
-      int page = -1;
-      if (kind == KIND_SHRINK) {
-        if (lane == 0) page = __ldg(p.slot_pages + slot * kMaxPagesPerSlot + g);
-      } else if (p.mode != MODE_SHRINK) {
-        if (lane < np) page = __ldg(p.slot_pages + slot * kMaxPagesPerSlot + lane);
-      }
       // bytes this stage will receive
       uint32_t a_bytes, act_bytes, n_adapter_copies;
       if (kind == KIND_SHRINK) {
@@ -298,45 +327,45 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
         m.kind = kind; m.job = job; m.pos0 = pos0; m.T = tcount; m.g = g; m.kc = kc; m.np = np;
         m.col0 = col0; m.ncols = ncols; m.nq = nq; m.p2 = p2; m.need = np * nkc;
       }
-      if (lane < tcount) m.rows[lane] = row;
+      // lane c issues copy c: adapter atoms first, then one activation row per token
+      const int ncopy = n_adapter_copies + tcount;
+      int row = 0, pg = 0;
+      const bool is_row = lane >= (int)n_adapter_copies && lane < ncopy;
+      if (is_row) {
+        const int pos = pos0 + lane - n_adapter_copies;
+        row = perm_smem ? (int)sm.perm[pos] : (p.perm ? __ldg(p.perm + pos) : pos);
+        m.rows[lane - n_adapter_copies] = row;
+      } else if (lane < (int)n_adapter_copies) {
+        const int gg = kind == KIND_SHRINK ? g : lane;
+        pg = pages_smem ? (int)sm.pages[sm.seg_pg[s] + gg] : __ldg(p.slot_pages + slot * kMaxPagesPerSlot + gg);
+      }
       __syncwarp();
       if (lane == 0)
         mbar_arrive_expect_tx(&sm.full[stage], a_bytes * n_adapter_copies + act_bytes * tcount);
       __syncwarp();
-      // issue copies: adapter copies on lanes [0, n_adapter_copies), activation rows after
-      const int ncopy = n_adapter_copies + tcount;
-      // (page ids / rows live in lanes; gather them explicitly with full-warp shuffles)
-      for (int base_c = 0; base_c < ncopy; base_c += 32) {
-        const int c = base_c + lane;
-        const int want_page_lane = kind == KIND_SHRINK ? 0 : min(c, 31);
-        const int pg = __shfl_sync(0xffffffffu, page, want_page_lane);
-        const int want_row_lane = min(max(c - (int)n_adapter_copies, 0), 31);
-        const int rw = __shfl_sync(0xffffffffu, row, want_row_lane);
-        if (c < ncopy) {
-          if (c < (int)n_adapter_copies) {
-            if (kind == KIND_SHRINK) {
-              const char* src = p.base + (long long)pg * p.page_bytes + jb.a_off +
-                                (long long)kc * ADAPTER_BYTES;
-              bulk_g2s(st, src, a_bytes, &sm.full[stage], pol_stream);
-            } else {
-              const char* src = p.base + (long long)pg * p.page_bytes + jb.b_off +
-                                (long long)(col0 * ES / kRowBytes) * kAtomBytes;
-              bulk_g2s(st + c * (nq * kRowBytes + PAGE_PAD), src, a_bytes, &sm.full[stage],
-                       pol_stream);
-            }
-          } else {
-            const int t = c - n_adapter_copies;
-            if (kind == KIND_SHRINK) {
-              const char* src = jb.x + ((long long)rw * p.h_in + (long long)kc * (ACT_ROW_BYTES / ES)) * ES;
-              bulk_g2s(st + ADAPTER_REGION + t * ACT_ROW_BYTES, src, act_bytes, &sm.full[stage],
-                       pol_act);
-            } else {
-              const char* src = jb.y + ((long long)rw * p.h_out + col0) * ES;
-              bulk_g2s(st + ADAPTER_REGION + t * ACT_ROW_BYTES, src, act_bytes, &sm.full[stage],
-                       pol_stream);
-            }
-          }
+      if (lane < (int)n_adapter_copies) {
+        if (kind == KIND_SHRINK) {
+          const char* src = p.base + (long long)pg * p.page_bytes + jb.a_off + (long long)kc * ADAPTER_BYTES;
+          bulk_g2s(st, src, a_bytes, &sm.full[stage], pol_stream);
+        } else {
+          const char* src = p.base + (long long)pg * p.page_bytes + jb.b_off +
+                            (long long)(col0 * ES / kRowBytes) * kAtomBytes;
+          bulk_g2s(st + lane * (nq * kRowBytes + PAGE_PAD), src, a_bytes, &sm.full[stage], pol_stream);
         }
+      } else if (is_row) {
+        const int t = lane - n_adapter_copies;
+        if (kind == KIND_SHRINK) {
+          const char* src = jb.x + ((long long)row * p.h_in + (long long)kc * (ACT_ROW_BYTES / ES)) * ES;
+          bulk_g2s(st + ADAPTER_REGION + t * ACT_ROW_BYTES, src, act_bytes, &sm.full[stage], pol_act);
+        } else {
+          const char* src = jb.y + ((long long)row * p.h_out + col0) * ES;
+          bulk_g2s(st + ADAPTER_REGION + t * ACT_ROW_BYTES, src, act_bytes, &sm.full[stage], pol_stream);
+        }
+      }
+      if (p.trace && lane == 0 && seq < p.trace_cap) {
+        unsigned long long* tr = p.trace + ((long long)blockIdx.x * p.trace_cap + seq) * 4;
+        tr[0] = gtimer();
+        tr[1] = ((unsigned long long)kind << 32) | (unsigned)(a_bytes * n_adapter_copies + act_bytes * tcount);
       }
       __syncwarp();
     }
@@ -351,6 +380,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
       mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
       const Meta m = sm.meta[stage];
       if (m.kind == KIND_END) break;
+      if (p.trace && ct == 0 && seq < p.trace_cap)
+        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 4 + 2] = gtimer();
       const unsigned char* st = sm.stage[stage];
       const Job& jb = p.jobs[m.job];
       if (m.kind == KIND_SHRINK) {
@@ -414,14 +445,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
             *dst = s;
           }
         }
-        __threadfence();
         named_bar_sync(bar_id, GROUP_THREADS);
         int* done = p.tile_done + (long long)m.job * p.max_tokens + m.pos0;
         if (p.mode == MODE_FUSED) {
-          if (ct == 0) red_release_gpu_add(done, 1);
+          // one thread publishes: the barrier orders the group's partial-sum stores before
+          // its cumulative release (gpu scope) of the tile counter
+          if (ct == 0) {
+            __threadfence();
+            red_release_gpu_add(done, 1);
+          }
         } else {
           // MODE_SHRINK: the last item of the tile folds the k-chunk partials into v_out
-          if (ct == 0) sm.flag[grp] = atom_acq_rel_gpu_add(done, 1) == m.need - 1;
+          if (ct == 0) {
+            __threadfence();
+            sm.flag[grp] = atom_acq_rel_gpu_add(done, 1) == m.need - 1;
+          }
           named_bar_sync(bar_id, GROUP_THREADS);
           if (sm.flag[grp]) {
             const int rows = min(m.np * kRowsPerPage, p.v_stride);
@@ -504,6 +542,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_decode_kernel(const __grid_c
           }
         }
       }
+      if (p.trace && ct == 0 && seq < p.trace_cap)
+        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 4 + 3] = gtimer();
       // release the stage (every consumer thread of the group arrives)
       mbar_arrive(&sm.empty[stage]);
     }
@@ -596,6 +636,8 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   prm.v_out = v_out;
   prm.v_in = v_in;
   prm.v_stride = v_stride;
+  prm.trace = pool->d_trace;
+  prm.trace_cap = pool->trace_cap;
   if (pool->dtype == CHAM_BF16) return launch<__nv_bfloat16>(pool, prm, (cudaStream_t)stream);
   return launch<float>(pool, prm, (cudaStream_t)stream);
 }

@@ -282,6 +282,13 @@ int cham_pool_fill_from_device(cham_pool* pool, int slot, const void* dev_src, s
   return fill_common(pool, slot, dev_src, bytes, stream, cudaMemcpyDeviceToDevice);
 }
 
+int cham_debug_set_trace(cham_pool* pool, void* dev_buf, int items_per_cta) {
+  if (!pool || (dev_buf && items_per_cta <= 0)) return fail(CHAM_ERR_INVALID, "cham_debug_set_trace: bad argument");
+  pool->d_trace = static_cast<unsigned long long*>(dev_buf);
+  pool->trace_cap = dev_buf ? items_per_cta : 0;
+  return CHAM_OK;
+}
+
 int cham_pool_copy_out(const cham_pool* pool, size_t offset, size_t bytes, void* dst, void* stream) {
   if (!pool || !dst) return fail(CHAM_ERR_INVALID, "cham_pool_copy_out: null argument");
   if (offset + bytes > (size_t)pool->n_pages * pool->page_bytes)

@@ -28,6 +28,8 @@ struct cham_pool {
   int* d_tile_done = nullptr;          // [kMaxJobs * max_tokens]
   float* d_vws = nullptr;              // [kMaxJobs][max_tokens][vws_kc][kMaxRank]
   int vws_kc = 1;
+  unsigned long long* d_trace = nullptr;  // debug timeline buffer (caller-owned)
+  int trace_cap = 0;
 };
 
 namespace cham {

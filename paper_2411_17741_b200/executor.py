@@ -1,0 +1,128 @@
+"""Step executor: the device-side replacement of the reference's LoRA cost seam.
+
+In the reference, one engine step is `(prefills, decoders) = (ready_prefills, decoding)`
+(engine.py:443-451) and its LoRA work is only *modelled* by CostModel.step_duration
+(engine.py:59-78).  `LoraStepExecutor` executes that work: it turns the batch descriptor
+into per-request (slot, rank, tokens) arrays, uploads them (pinned, async), builds the
+segment table on the device (K4) and runs `lora_apply` for every (layer, projection
+group).  The whole device part is stream-ordered and CUDA-graph capturable (the segment
+count never leaves the device), so a step replays as one graph.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .ops import SegmentTable, build_segments, lora_apply_multi, lora_apply_table
+from .pool import AdapterPool
+
+
+def batch_arrays(batch, slot_of: Callable[[str], int], rank_of: Callable[[str], int]):
+    """Per-request (slot, rank, tokens) arrays in batch order.
+
+    `batch` is either the engine's step tuple `(prefills, decoders)` — prefills contribute
+    `spec.input_tokens` tokens, decoders 1 token (engine.py:64-76) — or a list of admitted
+    requests (`BatchResult.admitted`, scheduler.py:246-255), which enter as prefills.
+    Objects are duck-typed: anything with `.spec.adapter_id` and `.spec.input_tokens`.
+    """
+    if isinstance(batch, tuple) and len(batch) == 2:
+        prefills, decoders = batch
+    else:
+        prefills, decoders = list(batch), []
+    slots, ranks, ntok = [], [], []
+    for r in prefills:
+        aid = r.spec.adapter_id
+        slots.append(slot_of(aid))
+        ranks.append(rank_of(aid))
+        ntok.append(int(r.spec.input_tokens))
+    for r in decoders:
+        aid = r.spec.adapter_id
+        slots.append(slot_of(aid))
+        ranks.append(rank_of(aid))
+        ntok.append(1)
+    return (np.asarray(slots, dtype=np.int32), np.asarray(ranks, dtype=np.int32),
+            np.asarray(ntok, dtype=np.int32))
+
+
+def adapter_units(batch, rank_of: Callable[[str], int]) -> int:
+    """The reference's `adapter_units` of a step (engine.py:64-76), as an integer."""
+    _, ranks, ntok = batch_arrays(batch, lambda a: 0, rank_of)
+    return int(np.sum(ranks.astype(np.int64) * ntok))
+
+
+class LoraStepExecutor:
+    """Runs one step's LoRA work on one replica.
+
+    proj_groups: projections that share their input activation and run in one launch
+    (e.g. [[0, 1, 2], [3]] for q/k/v + o); default: every projection on its own.
+    """
+
+    def __init__(self, pool: AdapterPool, max_requests: int = 4096, max_tokens: Optional[int] = None,
+                 proj_groups: Optional[Sequence[Sequence[int]]] = None, stream=None):
+        self.pool = pool
+        dev = pool.device
+        self.max_requests = min(int(max_requests), _lib.limits().max_requests)
+        self.max_tokens = int(max_tokens or pool.max_tokens)
+        self.proj_groups = [list(g) for g in (proj_groups or [[p] for p in range(pool.n_proj)])]
+        self.stream = stream
+        self.req_dev = torch.zeros(3, self.max_requests, dtype=torch.int32, device=dev)
+        self.req_host = torch.zeros(3, self.max_requests, dtype=torch.int32, pin_memory=True)
+        self.n_req = 0
+        self.table = SegmentTable(
+            perm=torch.zeros(self.max_tokens, dtype=torch.int32, device=dev),
+            seg_off=torch.zeros(self.max_requests + 1, dtype=torch.int32, device=dev),
+            seg_slot=torch.zeros(self.max_requests, dtype=torch.int32, device=dev),
+            seg_rank=torch.zeros(self.max_requests, dtype=torch.int32, device=dev),
+            n_seg=torch.zeros(1, dtype=torch.int32, device=dev),
+            n_tokens=self.max_tokens,
+        )
+
+    # -- host side ------------------------------------------------------------------------
+    def upload(self, req_slot, req_rank, req_ntok, stream=None) -> int:
+        """Stage the batch's request arrays in pinned memory and copy them asynchronously.
+        Returns the number of tokens of the batch."""
+        n = len(req_slot)
+        if n > self.max_requests:
+            raise ValueError(f"{n} requests > max_requests {self.max_requests}")
+        ntok = np.asarray(req_ntok, dtype=np.int64)
+        total = int(ntok.sum())
+        if total > self.max_tokens:
+            raise ValueError(f"{total} tokens > max_tokens {self.max_tokens}")
+        h = self.req_host.numpy()
+        h[0, :n] = req_slot
+        h[1, :n] = req_rank
+        h[2, :n] = req_ntok
+        s = stream or torch.cuda.current_stream(self.pool.device)
+        with torch.cuda.stream(s):
+            self.req_dev[:, :n].copy_(self.req_host[:, :n], non_blocking=True)
+        self.n_req = n
+        return total
+
+    # -- device side (capturable) ------------------------------------------------------------
+    def build(self, stream=None) -> SegmentTable:
+        n = self.n_req
+        build_segments(self.req_dev[0, :n], self.req_dev[1, :n], self.req_dev[2, :n], device=self.pool.device,
+                       stream=stream, out=self.table)
+        return self.table
+
+    def apply_layer(self, layer: int, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], stream=None):
+        """xs[g]: input of projection group g; ys[p]: output of projection p (in place)."""
+        for g, projs in enumerate(self.proj_groups):
+            if len(projs) == 1:
+                lora_apply_table(xs[g], ys[projs[0]], self.table, pool=self.pool, layer=layer, proj=projs[0],
+                                 stream=stream)
+            else:
+                lora_apply_multi([xs[g]] * len(projs), [ys[p] for p in projs], self.table, pool=self.pool,
+                                 layer=layer, projs=projs, stream=stream)
+
+    def launches_per_step(self) -> int:
+        return 1 + self.pool.n_layers * len(self.proj_groups)
+
+    def run(self, xs_per_layer, ys_per_layer, stream=None) -> None:
+        """K4 + every (layer, group) apply, on `stream`."""
+        self.build(stream)
+        for layer in range(self.pool.n_layers):
+            self.apply_layer(layer, xs_per_layer[layer], ys_per_layer[layer], stream)
