@@ -102,8 +102,8 @@ CHAM_API int cham_pool_fill_from_device(cham_pool* pool, int slot, const void* d
 CHAM_API int cham_pool_copy_out(const cham_pool* pool, size_t offset, size_t bytes, void* dst, void* stream);
 
 /* Debug: record a per-item timeline of the decode kernel into `dev_buf`
- * ([sm_count][items_per_cta][4] u64: producer issue ns, kind<<32|bytes, consumer start ns,
- * consumer end ns).  NULL disables.  Not for production use (adds global stores). */
+ * (2 x [sm_count][items_per_cta][8] u64 — shrink kernel then expand kernel: producer issue
+ * ns, kind<<32|bytes, consumer start ns, consumer end ns).  NULL disables.  Not for production use (adds global stores). */
 CHAM_API int cham_debug_set_trace(cham_pool* pool, void* dev_buf, int items_per_cta);
 
 /* Pack one adapter into page format on the host.  a: [n_layers][n_proj][h_in[p]][rank]

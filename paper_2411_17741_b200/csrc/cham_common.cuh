@@ -164,6 +164,11 @@ struct Elem<float> {
     return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
                       __float_as_uint(f[3]));
   }
+  // element pairs (2k, 2k+1) as float2, for packed FFMA2
+  __device__ static __forceinline__ void unpack2(const uint4& v, float2 (&f)[2]) {
+    f[0] = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
+    f[1] = make_float2(__uint_as_float(v.z), __uint_as_float(v.w));
+  }
 };
 template <>
 struct Elem<__nv_bfloat16> {
@@ -179,6 +184,12 @@ struct Elem<__nv_bfloat16> {
   __device__ static __forceinline__ uint4 pack(const float (&f)[8]) {
     return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
                       pack_bf16x2(f[6], f[7]));
+  }
+  __device__ static __forceinline__ void unpack2(const uint4& v, float2 (&f)[4]) {
+    f[0] = make_float2(bf_lo(v.x), bf_hi(v.x));
+    f[1] = make_float2(bf_lo(v.y), bf_hi(v.y));
+    f[2] = make_float2(bf_lo(v.z), bf_hi(v.z));
+    f[3] = make_float2(bf_lo(v.w), bf_hi(v.w));
   }
 };
 

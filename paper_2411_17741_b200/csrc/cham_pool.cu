@@ -159,7 +159,6 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_slot_pages);
     cudaFree(pool->d_slot_rank);
     cudaFree(pool->d_ctr);
-    cudaFree(pool->d_tile_done);
     cudaFree(pool->d_vws);
     delete pool;
     cudaSetDevice(prev);
@@ -177,17 +176,13 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   }
   e = cudaMalloc(&pool->d_slot_pages, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   if (e == cudaSuccess) e = cudaMalloc(&pool->d_slot_rank, sizeof(int) * (size_t)n_slots);
-  if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 8);
   if (e == cudaSuccess)
-    e = cudaMalloc(&pool->d_tile_done, sizeof(int) * (size_t)kMaxJobs * max_tokens);
-  if (e == cudaSuccess)
-    e = cudaMalloc(&pool->d_vws, sizeof(float) * (size_t)kMaxJobs * max_tokens * pool->vws_kc *
-                                     kMaxRank);
+    e = cudaMalloc(&pool->d_vws, 2 * sizeof(float) * (size_t)kMaxJobs * max_tokens * pool->vws_kc * kMaxRank);
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);
-  cudaMemset(pool->d_ctr, 0, sizeof(int) * 4);
-  cudaMemset(pool->d_tile_done, 0, sizeof(int) * (size_t)kMaxJobs * max_tokens);
+  cudaMemset(pool->d_ctr, 0, sizeof(int) * 8);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cleanup(CHAM_ERR_CUDA, std::string("cham_pool_create: ") + cudaGetErrorString(e));
   cudaSetDevice(prev);
@@ -202,7 +197,6 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_slot_pages);
   cudaFree(pool->d_slot_rank);
   cudaFree(pool->d_ctr);
-  cudaFree(pool->d_tile_done);
   cudaFree(pool->d_vws);
   delete pool;
   return CHAM_OK;

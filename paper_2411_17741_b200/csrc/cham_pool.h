@@ -24,10 +24,10 @@ struct cham_pool {
   std::vector<int> slot_rank;          // host mirror
   std::vector<int> slot_pages;         // host mirror [n_slots][kMaxPagesPerSlot]
   // decode / shrink / expand workspace (one launch at a time per pool)
-  int* d_ctr = nullptr;                // [0] item counter, [1] finished CTAs
-  int* d_tile_done = nullptr;          // [kMaxJobs * max_tokens]
-  float* d_vws = nullptr;              // [kMaxJobs][max_tokens][vws_kc][kMaxRank]
+  int* d_ctr = nullptr;                // [0,1] shrink: next item, finished CTAs; [2] error; [4,5] expand
+  float* d_vws = nullptr;              // 2 x [kMaxJobs][max_tokens][vws_kc][kMaxRank] (ping-pong)
   int vws_kc = 1;
+  unsigned long long apply_count = 0;  // selects the v ping-pong buffer
   unsigned long long* d_trace = nullptr;  // debug timeline buffer (caller-owned)
   int trace_cap = 0;
 };

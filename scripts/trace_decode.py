@@ -71,6 +71,14 @@ def analyze(tr, name):
     gaps = np.diff(np.sort(issue, axis=1), axis=1)
     gaps = np.diff(issue, axis=1)[valid[:, 1:] & valid[:, :-1]]
     print(f"  producer inter-issue gap us p50 {np.median(gaps)/1e3:.2f} p90 {np.percentile(gaps,90)/1e3:.2f}")
+    it = tr[:, :, 4] - t0
+    rd = tr[:, :, 5] - t0
+    pre = (rd - it)[valid]
+    post = (issue - rd)[valid]
+    print(f"  producer: iteration-start -> stage free us p50 {np.median(pre)/1e3:.2f} p90 {np.percentile(pre,90)/1e3:.2f}; "
+          f"stage free -> copies issued us p50 {np.median(post)/1e3:.2f} p90 {np.percentile(post,90)/1e3:.2f}")
+    prev_issue_to_it = (it[:, 1:] - issue[:, :-1])[valid[:, 1:] & valid[:, :-1]]
+    print(f"  producer: previous issue -> next iteration start us p50 {np.median(prev_issue_to_it)/1e3:.2f}")
     last_end = np.array([end[c, :per_cta[c]].max() if per_cta[c] else 0 for c in range(n_cta)])
     first_issue = np.array([issue[c, 0] for c in range(n_cta)])
     print(f"  CTA first-issue us p50 {np.median(first_issue)/1e3:.2f} max {first_issue.max()/1e3:.2f}; "
@@ -90,7 +98,7 @@ def main():
     torch.cuda.synchronize()
     cap = 512
     sm = torch.cuda.get_device_properties(0).multi_processor_count
-    buf = torch.zeros(sm, cap, 4, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(2, sm, cap, 8, dtype=torch.int64, device="cuda")
     _lib.call("cham_debug_set_trace", pool.handle, buf.data_ptr(), cap)
     out = ROOT / "gpurun_out"
     out.mkdir(exist_ok=True)
@@ -104,7 +112,12 @@ def main():
         torch.cuda.synchronize()
         tr = buf.cpu().numpy()
         np.save(out / f"trace_{name}.npy", tr)
-        analyze(tr, name)
+        t0 = tr[:, :, :, 0][tr[:, :, :, 0] > 0].min()
+        for k, kn in ((0, "shrink kernel"), (1, "expand kernel")):
+            sub = tr[k].copy()
+            valid = sub[:, :, 0] > 0
+            print(f"   [{kn}] starts {(sub[:, :, 0][valid].min() - t0) / 1e3:.1f} us after the first issue")
+            analyze(sub, f"{name} {kn}")
     _lib.call("cham_debug_set_trace", pool.handle, None, 0)
 
 
