@@ -319,7 +319,7 @@ def run_ours(args, rank: int, world: int):
             "adapter_read_frac_of_peak": adapter_bytes_step / (step_ms * 1e-3) / 1e9 / hbm_peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "kernel": "lora_decode_kernel<bf16> (fused shrink->expand)",
+                         "kernel": "lora_shrink_kernel<bf16> + lora_expand_kernel<bf16> (PDL pair per apply)",
                          "bytes_per_step": bytes_step, "launches_per_step": apply_launches,
                          "avg_launch_us": apply_ms * 1e3 / apply_launches,
                          "traffic": None},

@@ -139,12 +139,24 @@ CHAM_API int cham_build_segments(const int* req_slot, const int* req_rank, const
  *   pool's max_tokens.
  *   perm: grouped position -> token row (NULL = identity).
  *   n_seg >= 0: host segment count; n_seg < 0: read the count from n_seg_dev (device).
+ *   plan: optional launch plan from cham_build_plan for this segment table (NULL = the
+ *   kernels derive it themselves, at a few microseconds per launch).
  * Decode-sized segments run the fused shrink->expand GEMV kernel; segments of at least
  * prefill_min_tokens tokens in bf16 run the tcgen05 kernel.
  * ------------------------------------------------------------------------------------- */
 CHAM_API int cham_lora_apply(cham_pool* pool, int layer, int proj, const void* x, void* y,
                     int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
-                    const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream);
+                    const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream);
+
+/* Launch plan (segment prefix sums, largest-rank-first order, page ids, perm) for one
+ * segment table against the pool's current slot table, built on the device by one CTA.
+ * Valid while the slots of the batch stay bound (their adapters are pinned for the step),
+ * so one plan serves every (layer, projection) apply of a step.  `plan` is device memory of
+ * cham_plan_bytes() bytes, 16-byte aligned. */
+CHAM_API size_t cham_plan_bytes(void);
+CHAM_API int cham_build_plan(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
+                             const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan,
+                             void* stream);
 
 /* Several projections of one layer that share the token batch (e.g. q/k/v over the same
  * normed hidden state) in ONE launch.  All projections must have equal h_in and h_out. */
@@ -152,17 +164,17 @@ CHAM_API int cham_lora_apply_multi(cham_pool* pool, int layer, int n_jobs, const
                           const void* const* xs, void* const* ys, int n_tokens,
                           const int* perm,
                           const int* seg_off, const int* seg_slot, const int* seg_rank,
-                          int n_seg, const int* n_seg_dev, void* stream);
+                          int n_seg, const int* n_seg_dev, const void* plan, void* stream);
 
 /* Tensor-parallel halves (config C5).  shrink: v[k, 0:r] = x[perm[k]] . A_slot (fp32, rows
  * laid out [grouped position][v_stride]); expand: y[perm[k]] += v[k] . B_slot.  With A
  * sharded on h_in across ranks the caller all-reduces v between the two calls. */
 CHAM_API int cham_lora_shrink(cham_pool* pool, int layer, int proj, const void* x, float* v,
                      int v_stride, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
-                     const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream);
+                     const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream);
 CHAM_API int cham_lora_expand(cham_pool* pool, int layer, int proj, const float* v, int v_stride,
                      void* y, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
-                     const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream);
+                     const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream);
 
 #ifdef __cplusplus
 }

@@ -8,53 +8,52 @@
 // for every token t of segment s, y[t] += (x[t] . A_slot(s)) . B_slot(s).
 //
 // Design:
-//  * Work is cut into ~32 KiB items of adapter bytes.  K1 items = (job, tile, page,
-//    k-chunk); K2 items = (job, tile, column chunk); a tile is <= 4 tokens of one segment.
-//    CTA b owns the contiguous item range [b*N/G, (b+1)*N/G) and walks it with an
-//    incremental decoder (no per-item search, division or atomic).
-//  * Warp 0 is the producer: it decodes an item from a shared-memory plan (segments, page
-//    ids and perm are cached in smem, so the loop never waits on L2) and issues 1-D bulk
-//    async copies (TMA engine) into a 4-stage ring completing on mbarriers.  Weight tiles
-//    (A or B pages) do not depend on the previous kernel and are issued before
-//    griddepcontrol.wait; activations / v are issued after it.
-//  * Two consumer groups of 4 warps take alternate stages.  K1: every thread owns 16-byte
-//    k-columns of all 8 rank rows; fp32 FMAs; butterfly reduce-scatter across the warp;
-//    cross-warp sum -> v partial (fp32) in a ping-pong workspace.  K2: the stage holds the
-//    B atoms, the y rows and the tile's v partials; the group sums the k-chunk partials,
-//    FMAs against B, reduces across the sibling lanes holding other pages, adds into the
-//    staged y rows and stores y.  No separate elementwise kernel touches y.
-//  * K1 -> K2 ordering is the kernel boundary (griddepcontrol.wait in K2 before it copies
-//    v); no fences, flags or spin-waits inside either kernel.  Every CTA executes
-//    griddepcontrol.wait before exiting, so grid n completes after grid n-1 and the
+//  * A tile is <= 4 tokens of one segment.  Work is dispatched in *units* that loop over
+//    several pipeline stages (a K-loop), so every TMA bulk copy is large:
+//      K1 unit = (job, tile, page):  nkc stages, each = 32 KiB of A (8 rank rows x 2048
+//               bf16 of h_in) + the tile's x rows for that k-chunk; the 8 x T partial sums
+//               stay in registers across the stages, so v is written once, final.
+//      K2 unit = (job, tile, 1024-column chunk): ceil(np/2) stages, each = two pages x
+//               16 KiB of B; the y rows and the tile's v rows ride on the first stage.
+//  * Units are taken dynamically from a global counter (the next index is prefetched while
+//    the current unit streams).  K2 walks segments largest-rank first (LPT), so the tail
+//    is made of the small rank-8 units.
+//  * Warp 0 produces (plan in shared memory: no L2 round trips in the loop), 8 consumer
+//    warps compute with packed FFMA2 (fp32 accumulate).  Weights are issued before
+//    griddepcontrol.wait, activations / v after it; K2's dependency on K1 is the kernel
+//    boundary — no fences, flags or spin-waits inside a kernel.  Every CTA executes
+//    griddepcontrol.wait before exiting, so kernel n completes after kernel n-1 and the
 //    ping-pong v buffer of apply n-2 is free when apply n writes it.
 #include "cham_pool.h"
 
 namespace cham {
 namespace decode {
 
-constexpr int TG = 4;                       // tokens per tile
+constexpr int TG = 4;                        // tokens per tile
 constexpr int NSTAGE = 4;
-constexpr int ADAPTER_BYTES = 32768;        // adapter bytes per item
-constexpr int PAGE_PAD = 16;                // K2: per-page skew to spread smem banks
-constexpr int ACT_ROW_BYTES = ADAPTER_BYTES / kRowsPerPage;  // 4 KiB activations per token (K1)
-static_assert(ACT_ROW_BYTES == kActRowBytes, "pool workspace geometry");
-constexpr int Y_ROW_BYTES = 2048;           // K2: y bytes per token per item (<= 128 chunks)
-constexpr int V_BYTES = 8192;               // K2: staged v partials per item
-constexpr int K1_STAGE = ADAPTER_BYTES + TG * ACT_ROW_BYTES;
-constexpr int K2_B_REGION = ADAPTER_BYTES + kMaxPagesPerSlot * PAGE_PAD;
-constexpr int K2_STAGE = K2_B_REGION + TG * Y_ROW_BYTES + V_BYTES;
-constexpr int NGROUP = 1;                   // one consumer group: 3 stages in flight ahead of it
+constexpr int A_CHUNK = 32768;               // K1: adapter bytes per stage (8 rows x 4 KiB)
+constexpr int X_ROW = A_CHUNK / kRowsPerPage;  // K1: x bytes per token per stage (k-chunk)
+static_assert(X_ROW == kActRowBytes, "pool workspace geometry");
+constexpr int K1_STAGE = A_CHUNK + TG * X_ROW;
+constexpr int NC_BYTES = 2048;               // K2: bytes of one B row per unit (1024 bf16 columns)
+constexpr int NQ = NC_BYTES / 16;            // K2: 16-byte column chunks per unit (128)
+constexpr int PG = 2;                        // K2: pages per stage
+constexpr int B_PAGE = NC_BYTES * kRowsPerPage;  // 16 KiB
+constexpr int B_PITCH = B_PAGE + 64;         // skew the second page by 4 bank groups
+constexpr int K2_Y = PG * B_PITCH;
+constexpr int K2_V = K2_Y + TG * NC_BYTES;
+constexpr int K2_STAGE = K2_V + TG * kMaxRank * 4;
 constexpr int GROUP_WARPS = 8;
-constexpr int MAX_NQ = Y_ROW_BYTES / 16;    // K2: 16-byte column chunks per item
 constexpr int GROUP_THREADS = GROUP_WARPS * 32;
-constexpr int NTHREADS = 32 + NGROUP * GROUP_THREADS;
-constexpr int PLAN_SEGS = 512;              // segments per launch (plan lives in shared memory)
-constexpr int PLAN_PAGES = 2048;            // page ids cached in shared memory (else from L2)
-constexpr int PLAN_TOKENS = 2048;           // perm entries cached in shared memory (else from L2)
+constexpr int NTHREADS = 32 + GROUP_THREADS;
+static_assert(GROUP_THREADS == 2 * NQ, "K2 maps two threads per column chunk");
+constexpr int PLAN_SEGS = 512;
+constexpr int PLAN_PAGES = 2048;
+constexpr int PLAN_TOKENS = 2048;
 static_assert(PLAN_SEGS == kMaxSegments, "limits");
 
 enum Mode { MODE_FUSED = 0, MODE_SHRINK = 1, MODE_EXPAND = 2 };
-enum Kind { KIND_END = 0, KIND_SHRINK = 1, KIND_EXPAND = 2 };
+enum Kind { KIND_END = 0, KIND_WORK = 1 };
 
 struct Job {
   const char* x;
@@ -76,58 +75,67 @@ struct Params {
   const int* seg_rank;
   int n_seg;
   const int* n_seg_dev;
-  int* ctr;        // [0] next item, [1] finished CTAs (per kernel); ctr[2] of the pool = error
+  int* ctr;        // [0] next unit, [1] finished CTAs
   int* err;
-  float* vws;      // this apply's buffer: [job][max_tokens][vws_kc][kMaxRank]
-  int vws_kc;
+  float* vws;      // this apply's compact v buffer: [job][sum_s T_s * rpad_s]
+  long long vws_job_stride;
   int max_tokens;
-  const float* v_in;  // MODE_EXPAND: v [positions][v_stride] (kc = 1)
+  float* v_out;       // MODE_SHRINK: v [positions][v_stride]
+  const float* v_in;  // MODE_EXPAND: v [positions][v_stride]
   int v_stride;
-  unsigned long long* trace;  // debug: [cta][seq][4] globaltimer stamps (null = off)
+  unsigned long long* trace;  // debug: [cta][seq][8] globaltimer stamps (null = off)
   int trace_cap;
+  const void* plan;           // prebuilt Plan (cham_build_plan) or null: build in the kernel
 };
 
+// Per-stage record written by the producer, read by the consumers after the full barrier.
 struct Meta {
-  int kind, job, pos0, T, g, kc, np, col0, ncols, nq, p2, vrow;
+  int kind;
+  int nst;    // stages in this unit (set on every stage)
+  int job, seg, pos0, T, np;
+  int g;      // K1: page index of the unit
+  int kc;     // K1: k-chunk of this stage
+  int pg0;    // K2: first page of this stage
+  int npg;    // K2: pages in this stage (1 or 2)
+  int col0, ncols;
+  int vrow;   // K2: floats per staged v row
   int rows[TG];
 };
 
-struct Plan {
-  int sh_start[PLAN_SEGS + 1];
-  int ex_start[PLAN_SEGS + 1];
+struct alignas(16) Plan {
   int seg_off[PLAN_SEGS + 1];
-  int seg_pg[PLAN_SEGS + 1];  // prefix of pages per segment into `pages`
   int seg_sr[PLAN_SEGS];      // (slot << 9) | rank
-  int ex_cost_start[PLAN_SEGS + 1];  // prefix of expand cost (B bytes / 128) per job
+  int seg_pg[PLAN_SEGS + 1];  // prefix of pages -> pages[]
+  int v_start[PLAN_SEGS + 1]; // prefix of T_s * rpad_s -> compact v
+  int sh_start[PLAN_SEGS + 1];  // K1 units prefix (segment order)
+  int ex_start[PLAN_SEGS + 1];  // K2 tiles prefix (LPT order); units = tiles x column chunks
+  int order[PLAN_SEGS];         // K2 segment order: decreasing page count
+  int bucket[kMaxPagesPerSlot + 2];
   uint16_t pages[PLAN_PAGES];
   uint16_t perm[PLAN_TOKENS];
   int scan[NTHREADS / 32][4];
-  int totals[5];  // shrink items/job, expand items/job, tokens, pages, expand cost/job
+  int totals[6];  // K1 units/job, K2 tiles/job, tokens, pages, v floats/job, segments with work
+  int n_seg;
+  int pad;
 };
+static_assert(sizeof(Plan) % 16 == 0, "the plan is moved with one bulk copy");
 
 template <int STAGE_BYTES, int SCRATCH_BYTES>
 struct Shared {
   alignas(128) unsigned char stage[NSTAGE][STAGE_BYTES];
-  alignas(16) unsigned char scratch[NGROUP][SCRATCH_BYTES];
+  alignas(16) unsigned char scratch[SCRATCH_BYTES];
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
   Meta meta[NSTAGE];
+  uint64_t plan_bar;
   Plan plan;
-  int last_cta;
 };
 using K1Shared = Shared<K1_STAGE, GROUP_WARPS * 32 * 4>;
 using K2Shared = Shared<K2_STAGE, TG * kMaxRank * 4>;
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
-__host__ __device__ inline int pow2ceil(int v) {
-  int p = 1;
-  while (p < v) p <<= 1;
-  return p;
-}
-// K2 geometry for a segment with np pages: p2 = pow2ceil(np) sibling lanes share one
-// 16-byte column chunk (one page each); nq column chunks per item.
-__host__ __device__ inline int expand_p2(int np) { return pow2ceil(np); }
-__host__ __device__ inline int expand_nq(int p2) { return min(MAX_NQ, 256 / p2); }
+__host__ __device__ constexpr int cpow2(int v) { return v <= 1 ? 1 : 2 * cpow2((v + 1) / 2); }
+__host__ __device__ constexpr int clog2(int v) { return v <= 1 ? 0 : 1 + clog2(v / 2); }
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -139,40 +147,8 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Items per segment for K1 / K2, and the per-item K2 cost (B bytes / 128) used to
-// balance the expand work across CTAs.
-template <typename T>
-__device__ __forceinline__ void plan_counts(const Params& p, int T_s, int rank, int& n_sh, int& n_ex,
-                                            int& ex_cost) {
-  constexpr int ES = Elem<T>::kBytes;
-  constexpr int EPV = Elem<T>::kEPV;
-  const int np = ceil_div(rank, kRowsPerPage);
-  const int nt = ceil_div(T_s, TG);
-  if (np == 0 || nt == 0) {
-    n_sh = n_ex = ex_cost = 0;
-    return;
-  }
-  const int nkc = ceil_div(p.h_in * ES, ACT_ROW_BYTES);
-  const int nq = expand_nq(expand_p2(np));
-  n_sh = nt * np * nkc;
-  n_ex = nt * ceil_div(p.h_out, nq * EPV);
-  ex_cost = np * nq;
-}
-
-// index of the last segment s with start[s] <= v (start non-decreasing, start[0] = 0)
-__device__ __forceinline__ int seg_search(const int* start, int S, int v) {
-  int lo = 0, hi = S;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (start[mid] <= v) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-
 // Reduce-scatter of NV (power of two <= 32) per-lane partial sums across a warp: returns
-// the warp-wide sum of value index (lane >> (5 - log2 NV)).  Halving rounds first, then
-// plain xor rounds once every lane holds a single value.
+// the warp-wide sum of value index (lane >> (5 - log2 NV)).
 template <int NV>
 __device__ __forceinline__ float warp_reduce_scatter(float (&v)[NV], int lane) {
   int n = NV;
@@ -196,76 +172,101 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[NV], int lane) {
   return v[0];
 }
 
-__host__ __device__ constexpr int cpow2(int v) { return v <= 1 ? 1 : 2 * cpow2((v + 1) / 2); }
-__host__ __device__ constexpr int clog2(int v) { return v <= 1 ? 0 : 1 + clog2(v / 2); }
+// index of the last entry s in [0, S) with start[s] <= v (start non-decreasing)
+__device__ __forceinline__ int seg_search(const int* start, int S, int v) {
+  int lo = 0, hi = S;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (start[mid] <= v) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 
-// Builds the launch plan in shared memory (all threads).  Returns false on overflow.
 template <typename T>
+__device__ __forceinline__ int n_kchunks(const Params& p) {
+  return ceil_div(p.h_in * Elem<T>::kBytes, X_ROW);
+}
+template <typename T>
+__device__ __forceinline__ int n_colchunks(const Params& p) {
+  return ceil_div(p.h_out * Elem<T>::kBytes, NC_BYTES);
+}
+
+// Builds the launch plan in shared memory (all NTHREADS threads).  It depends only on the
+// segment table and the slot table, so one plan serves every (layer, projection) of a step.
 __device__ bool build_plan(const Params& p, Plan& pl, int S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kMaxPagesPerSlot + 2) pl.bucket[tid] = 0;
   const int per = ceil_div(S, NTHREADS);
   const int s0 = min(S, tid * per), s1 = min(S, s0 + per);
-  int lsh = 0, lex = 0, lpg = 0, lco = 0;
+  int lsh = 0, lpg = 0, lv = 0;
   for (int s = s0; s < s1; ++s) {
     const int o0 = p.seg_off[s], o1 = p.seg_off[s + 1];
     const int slot = p.seg_slot[s];
     const int rank = slot >= 0 ? min(p.seg_rank[s], kMaxRank) : 0;
     pl.seg_off[s] = o0;
     pl.seg_sr[s] = slot >= 0 ? ((slot << 9) | rank) : 0;
-    int a, b, c;
-    plan_counts<T>(p, o1 - o0, rank, a, b, c);
-    lsh += a;
-    lex += b;
-    lpg += ceil_div(rank, kRowsPerPage);
-    lco += b * c;
+    const int np = ceil_div(rank, kRowsPerPage);
+    const int nt = ceil_div(o1 - o0, TG);
+    lsh += nt * np;
+    lpg += np;
+    lv += (o1 - o0) * np * kRowsPerPage;
   }
-  int ish = lsh, iex = lex, ipg = lpg, ico = lco;
+  int ish = lsh, ipg = lpg, iv = lv;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int a = __shfl_up_sync(0xffffffffu, ish, o);
-    const int b = __shfl_up_sync(0xffffffffu, iex, o);
     const int c = __shfl_up_sync(0xffffffffu, ipg, o);
-    const int d = __shfl_up_sync(0xffffffffu, ico, o);
-    if (lane >= o) { ish += a; iex += b; ipg += c; ico += d; }
+    const int d = __shfl_up_sync(0xffffffffu, iv, o);
+    if (lane >= o) { ish += a; ipg += c; iv += d; }
   }
-  if (lane == 31) { pl.scan[warp][0] = ish; pl.scan[warp][1] = iex; pl.scan[warp][2] = ipg; pl.scan[warp][3] = ico; }
+  if (lane == 31) { pl.scan[warp][0] = ish; pl.scan[warp][1] = ipg; pl.scan[warp][2] = iv; }
   __syncthreads();
-  int bsh = 0, bex = 0, bpg = 0, bco = 0;
-  for (int w = 0; w < warp; ++w) {
-    bsh += pl.scan[w][0]; bex += pl.scan[w][1]; bpg += pl.scan[w][2]; bco += pl.scan[w][3];
-  }
+  int bsh = 0, bpg = 0, bv = 0;
+  for (int w = 0; w < warp; ++w) { bsh += pl.scan[w][0]; bpg += pl.scan[w][1]; bv += pl.scan[w][2]; }
   bsh += ish - lsh;
-  bex += iex - lex;
   bpg += ipg - lpg;
-  bco += ico - lco;
+  bv += iv - lv;
   for (int s = s0; s < s1; ++s) {
-    const int rank = pl.seg_sr[s] & 511;
-    int a, b, c;
-    plan_counts<T>(p, p.seg_off[s + 1] - pl.seg_off[s], rank, a, b, c);
+    const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+    const int T_s = p.seg_off[s + 1] - pl.seg_off[s];
     pl.sh_start[s] = bsh;
-    pl.ex_start[s] = bex;
     pl.seg_pg[s] = bpg;
-    pl.ex_cost_start[s] = bco;
-    bsh += a;
-    bex += b;
-    bpg += ceil_div(rank, kRowsPerPage);
-    bco += b * c;
+    pl.v_start[s] = bv;
+    bsh += ceil_div(T_s, TG) * np;
+    bpg += np;
+    bv += T_s * np * kRowsPerPage;
+    if (np > 0 && T_s > 0) atomicAdd(&pl.bucket[np], 1);
   }
   if (tid == NTHREADS - 1) {
     pl.sh_start[S] = bsh;
-    pl.ex_start[S] = bex;
     pl.seg_pg[S] = bpg;
-    pl.ex_cost_start[S] = bco;
-    pl.totals[4] = bco;
+    pl.v_start[S] = bv;
     const int ntok = S > 0 ? p.seg_off[S] : 0;
     pl.seg_off[S] = ntok;
     pl.totals[0] = bsh;
-    pl.totals[1] = bex;
     pl.totals[2] = ntok;
     pl.totals[3] = bpg;
+    pl.totals[4] = bv;
+    pl.n_seg = S;
   }
   __syncthreads();
   if (pl.totals[2] > p.max_tokens) return false;
+  // LPT order for K2: bucket offsets by decreasing page count, then scatter segments
+  if (tid == 0) {
+    int acc = 0;
+    for (int np = kMaxPagesPerSlot; np >= 1; --np) {
+      const int c = pl.bucket[np];
+      pl.bucket[np] = acc;
+      acc += c;
+    }
+    pl.totals[5] = acc;  // segments with work
+  }
+  __syncthreads();
+  for (int s = s0; s < s1; ++s) {
+    const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+    const int T_s = pl.seg_off[s + 1] - pl.seg_off[s];
+    if (np > 0 && T_s > 0) pl.order[atomicAdd(&pl.bucket[np], 1)] = s;
+  }
   if (pl.totals[3] <= PLAN_PAGES) {
     for (int s = s0; s < s1; ++s) {
       const int slot = pl.seg_sr[s] >> 9;
@@ -279,19 +280,33 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S) {
       pl.perm[i] = (uint16_t)(p.perm ? __ldg(p.perm + i) : i);
   }
   __syncthreads();
+  // K2 unit prefix over the LPT order (one warp scans; <= 512 entries)
+  const int nw = pl.totals[5];
+  if (warp == 0) {
+    int carry = 0;
+    for (int base = 0; base < nw; base += 32) {
+      const int i = base + lane;
+      int u = 0;
+      if (i < nw) {
+        const int s = pl.order[i];
+        u = ceil_div(pl.seg_off[s + 1] - pl.seg_off[s], TG);
+      }
+      int inc = u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += a;
+      }
+      if (i < nw) pl.ex_start[i] = carry + inc - u;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      pl.ex_start[nw] = carry;
+      pl.totals[1] = carry;
+    }
+  }
+  __syncthreads();
   return true;
-}
-
-struct ItemPos {
-  int job, s, local;
-};
-__device__ __forceinline__ ItemPos locate(const int* start, int per_job, int S, int item) {
-  ItemPos ip;
-  ip.job = item / per_job;
-  const int rem = item - ip.job * per_job;
-  ip.s = seg_search(start, S, rem);
-  ip.local = rem - start[ip.s];
-  return ip;
 }
 
 __device__ __forceinline__ int page_of(const Params& p, const Plan& pl, bool pages_smem, int s, int slot, int g) {
@@ -301,31 +316,53 @@ __device__ __forceinline__ int row_of(const Params& p, const Plan& pl, bool perm
   return perm_smem ? (int)pl.perm[pos] : (p.perm ? __ldg(p.perm + pos) : pos);
 }
 
-// Two END markers (one per consumer group) at sequence numbers seq and seq + 1.
 template <class SH>
 __device__ __forceinline__ void post_end(SH& sm, int seq) {
-  for (int k = 0; k < NGROUP; ++k) {
-    const int sq = seq + k, st = sq % NSTAGE;
-    mbar_wait(&sm.empty[st], ((sq / NSTAGE) & 1) ^ 1);
-    sm.meta[st].kind = KIND_END;
-    mbar_arrive(&sm.full[st]);
+  const int st = seq % NSTAGE;
+  mbar_wait(&sm.empty[st], ((seq / NSTAGE) & 1) ^ 1);
+  sm.meta[st].kind = KIND_END;
+  mbar_arrive(&sm.full[st]);
+}
+
+// The last CTA to finish re-arms the unit counter for the next launch of this kernel.
+__device__ __forceinline__ void reset_counter_if_last(const Params& p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
   }
 }
 
+// Barriers + plan.  A prebuilt plan is pulled into shared memory with one bulk copy (the
+// plan is written by an earlier kernel of the step, so it may be read before the PDL wait).
 template <class SH>
 __device__ __forceinline__ bool prologue(const Params& p, SH& sm, int& S_out) {
-  const int tid = threadIdx.x;
-  const int S = p.n_seg >= 0 ? p.n_seg : *p.n_seg_dev;
-  S_out = S;
-  if (S > PLAN_SEGS || S < 0) return false;
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], GROUP_THREADS);
     }
+    mbar_init(&sm.plan_bar, 1);
     fence_mbar_init();
+    if (p.plan) {
+      mbar_arrive_expect_tx(&sm.plan_bar, sizeof(Plan));
+      bulk_g2s(&sm.plan, p.plan, sizeof(Plan), &sm.plan_bar, policy_evict_last());
+    }
   }
-  return true;
+  __syncthreads();
+  if (p.plan) {
+    mbar_wait(&sm.plan_bar, 0);
+    S_out = sm.plan.totals[5] >= 0 ? 1 : 0;  // unused with a prebuilt plan
+    return sm.plan.totals[2] <= p.max_tokens;
+  }
+  const int S = p.n_seg >= 0 ? p.n_seg : *p.n_seg_dev;
+  S_out = S;
+  if (S > PLAN_SEGS || S < 0) return false;
+  return build_plan(p, sm.plan, S);
 }
 
 __device__ __forceinline__ void abort_launch(const Params& p) {
@@ -333,42 +370,62 @@ __device__ __forceinline__ void abort_launch(const Params& p) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
 }
 
+__device__ __forceinline__ void trace_producer(const Params& p, int seq, unsigned long long t_it,
+                                               unsigned long long t_ready, int kind, uint32_t bytes) {
+  if (p.trace && seq < p.trace_cap) {
+    unsigned long long* tr = p.trace + ((long long)blockIdx.x * p.trace_cap + seq) * 8;
+    tr[0] = gtimer();
+    tr[1] = ((unsigned long long)kind << 32) | bytes;
+    tr[4] = t_it;
+    tr[5] = t_ready;
+  }
+}
+__device__ __forceinline__ void trace_consumer(const Params& p, int seq, int field) {
+  if (p.trace && seq < p.trace_cap) p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + field] = gtimer();
+}
 
-// K1 consumer work for one item with NT (1..4) tokens: partial v rows [g*8, g*8+8) for
-// k-chunk kc.  Releases the stage as soon as its shared memory has been read.
+// =========================================================================== K1: shrink
+// One unit: nst stages (k-chunks) of one page of one tile; the consumers keep the 8 x NT
+// dot products in registers across the stages and write the final v rows at the end.
 template <typename T, int NT>
-__device__ __forceinline__ void shrink_item(const Params& p, const Meta& m, const unsigned char* st,
-                                            uint64_t* empty_bar, float* red, int ct, int lane, int gw,
-                                            int bar_id) {
+__device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1Shared& sm, int& seq, const Meta& m0,
+                                            float* red, int ct, int lane, int gw) {
   constexpr int ES = Elem<T>::kBytes;
   constexpr int EPV = Elem<T>::kEPV;
   constexpr int NP2 = EPV / 2;
-  constexpr int NTR = cpow2(NT);                  // tokens padded to a power of two
-  constexpr int NV = kRowsPerPage * NTR;          // values reduced per item
+  constexpr int NTR = cpow2(NT);
+  constexpr int NV = kRowsPerPage * NTR;
   float2 acc2[kRowsPerPage][NT];
 #pragma unroll
   for (int j = 0; j < kRowsPerPage; ++j)
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc2[j][t] = make_float2(0.f, 0.f);
-  const int kbytes = min(ACT_ROW_BYTES, p.h_in * ES - m.kc * ACT_ROW_BYTES);
-  const int nqk = kbytes >> 4;
-  const unsigned char* X = st + ADAPTER_BYTES;
-  for (int q = ct; q < nqk; q += GROUP_THREADS) {
-    const int a = q >> 3, c = q & 7;
-    float2 xf[NT][NP2];
+  for (int k = 0; k < m0.nst; ++k, ++seq) {
+    const int stage = seq % NSTAGE;
+    if (k > 0) mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
+    if (ct == 0) trace_consumer(p, seq, 2);
+    const Meta& m = sm.meta[stage];
+    const unsigned char* st = sm.stage[stage];
+    const int kbytes = min(X_ROW, p.h_in * ES - m.kc * X_ROW);
+    const unsigned char* X = st + A_CHUNK;
+    for (int q = ct; q < (kbytes >> 4); q += GROUP_THREADS) {
+      const int a = q >> 3, c = q & 7;
+      float2 xf[NT][NP2];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) Elem<T>::unpack2(lds128(X + t * ACT_ROW_BYTES + q * 16), xf[t]);
+      for (int t = 0; t < NT; ++t) Elem<T>::unpack2(lds128(X + t * X_ROW + q * 16), xf[t]);
 #pragma unroll
-    for (int j = 0; j < kRowsPerPage; ++j) {
-      float2 af[NP2];
-      Elem<T>::unpack2(lds128(st + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), af);
+      for (int j = 0; j < kRowsPerPage; ++j) {
+        float2 af[NP2];
+        Elem<T>::unpack2(lds128(st + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), af);
 #pragma unroll
-      for (int k = 0; k < NP2; ++k)
+        for (int e = 0; e < NP2; ++e)
 #pragma unroll
-        for (int t = 0; t < NT; ++t) acc2[j][t] = __ffma2_rn(af[k], xf[t][k], acc2[j][t]);
+          for (int t = 0; t < NT; ++t) acc2[j][t] = __ffma2_rn(af[e], xf[t][e], acc2[j][t]);
+      }
     }
+    if (ct == 0) trace_consumer(p, seq, 3);
+    mbar_arrive(&sm.empty[stage]);  // this stage has been read: hand it back
   }
-  mbar_arrive(empty_bar);  // the stage has been read: hand it back to the producer
   float v[NV];
 #pragma unroll
   for (int j = 0; j < kRowsPerPage; ++j)
@@ -376,427 +433,351 @@ __device__ __forceinline__ void shrink_item(const Params& p, const Meta& m, cons
     for (int t = 0; t < NTR; ++t) v[j * NTR + t] = t < NT ? acc2[j][t].x + acc2[j][t].y : 0.f;
   const float mine = warp_reduce_scatter<NV>(v, lane);
   constexpr int SHIFT = 5 - clog2(NV);
-  named_bar_sync(bar_id, GROUP_THREADS);  // previous item's readers of `red` are done
+  named_bar_sync(1, GROUP_THREADS);  // the previous unit's readers of `red` are done
   if ((lane & ((1 << SHIFT) - 1)) == 0) red[gw * 32 + (lane >> SHIFT)] = mine;
-  named_bar_sync(bar_id, GROUP_THREADS);
+  named_bar_sync(1, GROUP_THREADS);
   if (ct < NV) {
     float sum = 0.f;
 #pragma unroll
     for (int w2 = 0; w2 < GROUP_WARPS; ++w2) sum += red[w2 * 32 + ct];
     const int j = ct / NTR, t = ct % NTR;
-    if (t < NT)
-      p.vws[(((long long)m.job * p.max_tokens + m.pos0 + t) * p.vws_kc + m.kc) * kMaxRank + m.g * kRowsPerPage + j] =
-          sum;
-  }
-}
-
-// K2 consumer work for one item with NT (1..4) tokens.
-template <typename T, int NT>
-__device__ __forceinline__ void expand_item(const Params& p, const Meta& m, const unsigned char* st, float* vs,
-                                            int nkc, int ct, int bar_id) {
-  constexpr int ES = Elem<T>::kBytes;
-  constexpr int EPV = Elem<T>::kEPV;
-  constexpr int NP2 = EPV / 2;
-  const int rows = m.np * kRowsPerPage;
-  const bool v_staged = m.vrow > 0;
-  const int vrow = v_staged ? m.vrow : -m.vrow;
-  named_bar_sync(bar_id, GROUP_THREADS);  // previous item's readers of vs are done
-  const float* Vs = reinterpret_cast<const float*>(st + K2_B_REGION + TG * Y_ROW_BYTES);
-  for (int idx = ct; idx < NT * rows; idx += GROUP_THREADS) {
-    const int t = idx / rows, r = idx - t * rows;
-    float sum = 0.f;
-    if (r < vrow) {
-      for (int k2 = 0; k2 < nkc; ++k2) {
-        if (v_staged) {
-          sum += Vs[(t * nkc + k2) * vrow + r];
-        } else if (p.v_in) {
-          sum += __ldg(p.v_in + (long long)(m.pos0 + t) * p.v_stride + r);
-        } else {
-          sum += __ldg(p.vws + (((long long)m.job * p.max_tokens + m.pos0 + t) * p.vws_kc + k2) * kMaxRank + r);
-        }
-      }
-    }
-    vs[t * kMaxRank + r] = sum;
-  }
-  named_bar_sync(bar_id, GROUP_THREADS);
-  const int p2 = m.p2;
-  const int gi = ct & (p2 - 1);
-  const int q = ct / p2;  // threads with q >= nq idle in the FMA phase (rank-8 items)
-  float2 acc[NT][NP2];
-#pragma unroll
-  for (int t = 0; t < NT; ++t)
-#pragma unroll
-    for (int k = 0; k < NP2; ++k) acc[t][k] = make_float2(0.f, 0.f);
-  const bool active = q < m.nq && q * EPV < m.ncols;
-  if (active) {
-    const int a = q >> 3, c = q & 7;
-    for (int g = gi; g < m.np; g += p2) {
-      const unsigned char* Bg = st + g * (m.nq * kRowBytes + PAGE_PAD);
-      float vv[NT][kRowsPerPage];  // v[t][g*8 .. g*8+7]: two 16-byte loads per token
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const float4 lo = *reinterpret_cast<const float4*>(vs + t * kMaxRank + g * kRowsPerPage);
-        const float4 hi = *reinterpret_cast<const float4*>(vs + t * kMaxRank + g * kRowsPerPage + 4);
-        vv[t][0] = lo.x; vv[t][1] = lo.y; vv[t][2] = lo.z; vv[t][3] = lo.w;
-        vv[t][4] = hi.x; vv[t][5] = hi.y; vv[t][6] = hi.z; vv[t][7] = hi.w;
-      }
-#pragma unroll
-      for (int j = 0; j < kRowsPerPage; ++j) {
-        float2 bf[NP2];
-        Elem<T>::unpack2(lds128(Bg + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const float2 v2 = make_float2(vv[t][j], vv[t][j]);
-#pragma unroll
-          for (int k = 0; k < NP2; ++k) acc[t][k] = __ffma2_rn(v2, bf[k], acc[t][k]);
-        }
-      }
-    }
-  }
-  for (int o = 1; o < p2; o <<= 1) {
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int k = 0; k < NP2; ++k) {
-        acc[t][k].x += __shfl_xor_sync(0xffffffffu, acc[t][k].x, o);
-        acc[t][k].y += __shfl_xor_sync(0xffffffffu, acc[t][k].y, o);
-      }
-  }
-  if (active) {
-    const unsigned char* Y = st + K2_B_REGION;
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      // the p2 sibling lanes hold identical sums; lane gi stores tokens t == gi (mod p2)
-      if ((t & (p2 - 1)) == gi) {
-        float yf[EPV];
-        Elem<T>::unpack(lds128(Y + t * Y_ROW_BYTES + q * 16), yf);
-#pragma unroll
-        for (int k = 0; k < NP2; ++k) {
-          yf[2 * k] += acc[t][k].x;
-          yf[2 * k + 1] += acc[t][k].y;
-        }
-        char* dst = p.jobs[m.job].y + ((long long)m.rows[t] * p.h_out + m.col0) * ES + q * 16;
-        *reinterpret_cast<uint4*>(dst) = Elem<T>::pack(yf);
+    if (t < NT) {
+      const int row = m0.g * kRowsPerPage + j;
+      if (p.v_out) {
+        p.v_out[(long long)(m0.pos0 + t) * p.v_stride + row] = sum;  // TP layout [position][v_stride]
+      } else {
+        const int rpad = m0.np * kRowsPerPage;
+        const int t_seg = m0.pos0 + t - pl.seg_off[m0.seg];
+        p.vws[m0.job * p.vws_job_stride + pl.v_start[m0.seg] + t_seg * rpad + row] = sum;
       }
     }
   }
 }
 
-// =========================================================================== K1: shrink
 template <typename T>
 __global__ void __launch_bounds__(NTHREADS, 1) lora_shrink_kernel(const __grid_constant__ Params p) {
   constexpr int ES = Elem<T>::kBytes;
-  constexpr int EPV = Elem<T>::kEPV;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   K1Shared& sm = *reinterpret_cast<K1Shared*>(smem_raw);
   Plan& pl = sm.plan;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int S;
-  if (!prologue(p, sm, S) || !build_plan<T>(p, pl, S)) {
+  if (!prologue(p, sm, S)) {
     abort_launch(p);
     return;
   }
-  const int SH = pl.totals[0];
+  S = pl.n_seg;
+  const int US = pl.totals[0];
   const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
   const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
-  const int total = p.n_jobs * SH;
-  const int nkc = ceil_div(p.h_in * ES, ACT_ROW_BYTES);
+  const int total = p.n_jobs * US;
+  const int nkc = n_kchunks<T>(p);
   const int natoms = p.h_in * ES / kRowBytes;
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
-    const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page item
-    // this CTA's contiguous share of the item space, walked with an incremental decoder
-    const int i0 = (int)((long long)total * blockIdx.x / gridDim.x);
-    const int i1 = (int)((long long)total * (blockIdx.x + 1) / gridDim.x);
-    int job = 0, s = 0, tile = 0, g = 0, kc = 0;
-    int o0 = 0, Ts = 0, slot = 0, np = 0, nt = 0;
-    auto load_seg = [&]() {
-      o0 = pl.seg_off[s];
-      Ts = pl.seg_off[s + 1] - o0;
-      slot = pl.seg_sr[s] >> 9;
-      np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
-      nt = ceil_div(Ts, TG);
-    };
-    if (i0 < i1) {
-      const ItemPos ip = locate(pl.sh_start, SH, S, i0);
-      job = ip.job;
-      s = ip.s;
-      load_seg();
-      const int per_tile = np * nkc;
-      tile = ip.local / per_tile;
-      const int r2 = ip.local - tile * per_tile;
-      g = r2 / nkc;
-      kc = r2 - g * nkc;
-    }
+    const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page of the tile
     bool waited = false;
     int seq = 0;
-    for (int item = i0; item < i1; ++item, ++seq) {
-      const unsigned long long t_it = p.trace ? gtimer() : 0;
-      const int stage = seq % NSTAGE;
+    int next = 0;
+    if (lane == 0) next = atomicAdd(p.ctr, 1);
+    for (;;) {
+      const int unit = __shfl_sync(0xffffffffu, next, 0);
+      if (unit >= total) break;
+      if (lane == 0) next = atomicAdd(p.ctr, 1);  // prefetch the next unit index
+      const int job = unit / US;
+      const int rem = unit - job * US;
+      const int s = seg_search(pl.sh_start, S, rem);
+      const int local = rem - pl.sh_start[s];
+      const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
+      const int slot = pl.seg_sr[s] >> 9;
+      const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+      const int tile = local / np, g = local - tile * np;
       const int pos0 = o0 + tile * TG;
       const int tcount = min(TG, Ts - tile * TG);
-      const int a0 = kc * (ADAPTER_BYTES / kAtomBytes);
-      const uint32_t a_bytes = min(ADAPTER_BYTES / kAtomBytes, natoms - a0) * kAtomBytes;
-      const uint32_t x_bytes = a_bytes / kRowsPerPage;
       const Job& jb = p.jobs[job];
-      unsigned char* st = sm.stage[stage];
-      int row = 0, pg = 0;
+      int row = 0;
       if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
-      if (lane == 0) pg = page_of(p, pl, pages_smem, s, slot, g);
-      if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
-      const unsigned long long t_ready = p.trace ? gtimer() : 0;
-      __syncwarp();
-      Meta& m = sm.meta[stage];
-      if (lane == 0) {
-        m.kind = KIND_SHRINK; m.job = job; m.pos0 = pos0; m.T = tcount; m.g = g; m.kc = kc; m.np = np;
-        mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
-        bulk_g2s(st, p.base + (long long)pg * p.page_bytes + jb.a_off + (long long)a0 * kAtomBytes, a_bytes,
-                 &sm.full[stage], pol_w);
-      }
-      if (!waited) {  // x may be produced by the previous kernel
-        pdl_wait();
-        pdl_launch_dependents();
-        waited = true;
-      }
-      if (lane < tcount) {
-        const char* src = jb.x + ((long long)row * p.h_in + (long long)kc * (ACT_ROW_BYTES / ES)) * ES;
-        bulk_g2s(st + ADAPTER_BYTES + lane * ACT_ROW_BYTES, src, x_bytes, &sm.full[stage], pol_x);
-      }
-      if (p.trace && lane == 0 && seq < p.trace_cap) {
-        unsigned long long* tr = p.trace + ((long long)blockIdx.x * p.trace_cap + seq) * 8;
-        tr[0] = gtimer();
-        tr[1] = (1ull << 32) | (a_bytes + x_bytes * tcount);
-        tr[4] = t_it;
-        tr[5] = t_ready;
-      }
-      // advance (kc fastest, then page, tile, segment, job)
-      if (++kc == nkc) {
-        kc = 0;
-        if (++g == np) {
-          g = 0;
-          if (++tile == nt) {
-            tile = 0;
-            do {
-              if (++s == S) { s = 0; ++job; }
-            } while (job < p.n_jobs && pl.sh_start[s + 1] == pl.sh_start[s]);
-            if (job < p.n_jobs) load_seg();
-          }
+      const int pg = page_of(p, pl, pages_smem, s, slot, g);
+      const char* a_src = p.base + (long long)pg * p.page_bytes + jb.a_off;
+      for (int kc = 0; kc < nkc; ++kc, ++seq) {
+        const unsigned long long t_it = p.trace ? gtimer() : 0;
+        const int stage = seq % NSTAGE;
+        const int a0 = kc * (A_CHUNK / kAtomBytes);
+        const uint32_t a_bytes = min(A_CHUNK / kAtomBytes, natoms - a0) * kAtomBytes;
+        const uint32_t x_bytes = a_bytes / kRowsPerPage;
+        unsigned char* st = sm.stage[stage];
+        if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+        const unsigned long long t_ready = p.trace ? gtimer() : 0;
+        __syncwarp();
+        Meta& m = sm.meta[stage];
+        if (lane == 0) {
+          m.kind = KIND_WORK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+          m.g = g; m.kc = kc;
+          mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
+          bulk_g2s(st, a_src + (long long)a0 * kAtomBytes, a_bytes, &sm.full[stage], pol_w);
         }
+        if (lane < tcount) m.rows[lane] = row;
+        if (!waited) {  // x may be produced by the previous kernel
+          pdl_wait();
+          pdl_launch_dependents();
+          waited = true;
+        }
+        if (lane < tcount)
+          bulk_g2s(st + A_CHUNK + lane * X_ROW, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
+                   &sm.full[stage], pol_x);
+        if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
+        __syncwarp();
       }
-      __syncwarp();
     }
     if (!waited) pdl_wait();
     if (lane == 0) post_end(sm, seq);
   } else {
     // ------------------------------------------------------------------ consumers
-    const int grp = (warp - 1) / GROUP_WARPS;
-    const int ct = tid - 32 - grp * GROUP_THREADS;
+    const int ct = tid - 32;
     const int gw = ct >> 5;
-    const int bar_id = 1 + grp;
-    float* red = reinterpret_cast<float*>(sm.scratch[grp]);
-    for (int seq = grp;; seq += NGROUP) {
+    float* red = reinterpret_cast<float*>(sm.scratch);
+    int seq = 0;
+    for (;;) {
       const int stage = seq % NSTAGE;
       mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
-      const Meta m = sm.meta[stage];
-      if (m.kind == KIND_END) break;
-      if (p.trace && ct == 0 && seq < p.trace_cap)
-        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 2] = gtimer();
-      const unsigned char* st = sm.stage[stage];
-      switch (m.T) {
-        case 1: shrink_item<T, 1>(p, m, st, &sm.empty[stage], red, ct, lane, gw, bar_id); break;
-        case 2: shrink_item<T, 2>(p, m, st, &sm.empty[stage], red, ct, lane, gw, bar_id); break;
-        case 3: shrink_item<T, 3>(p, m, st, &sm.empty[stage], red, ct, lane, gw, bar_id); break;
-        default: shrink_item<T, 4>(p, m, st, &sm.empty[stage], red, ct, lane, gw, bar_id); break;
+      const Meta m0 = sm.meta[stage];
+      if (m0.kind == KIND_END) break;
+      switch (m0.T) {
+        case 1: shrink_unit<T, 1>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
+        case 2: shrink_unit<T, 2>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
+        case 3: shrink_unit<T, 3>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
+        default: shrink_unit<T, 4>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
       }
-      if (p.trace && ct == 0 && seq < p.trace_cap)
-        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 3] = gtimer();
+    }
+  }
+  reset_counter_if_last(p);
+}
+
+// =========================================================================== K2: expand
+// One unit: output tile [NT tokens x 1024 columns]; stages walk the adapter's pages two at
+// a time.  Thread (q, h) owns 16-byte column chunk q (= ct >> 1) and page / half-page h.
+template <typename T, int NT>
+__device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& seq, const Meta& m0, int ct) {
+  constexpr int ES = Elem<T>::kBytes;
+  constexpr int EPV = Elem<T>::kEPV;
+  constexpr int NP2 = EPV / 2;
+  float* vs = reinterpret_cast<float*>(sm.scratch);  // [TG][kMaxRank]
+  const int q = ct >> 1, h = ct & 1;
+  const int a = q >> 3, c = q & 7;
+  const int rows = m0.np * kRowsPerPage;
+  const bool active = q * EPV < m0.ncols;
+  float2 acc[NT][NP2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int e = 0; e < NP2; ++e) acc[t][e] = make_float2(0.f, 0.f);
+  float yv[NT][EPV];  // this thread's share of the y rows (staged with the first stage)
+  for (int k = 0; k < m0.nst; ++k, ++seq) {
+    const int stage = seq % NSTAGE;
+    if (k > 0) mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
+    if (ct == 0) trace_consumer(p, seq, 2);
+    const Meta& m = sm.meta[stage];
+    const unsigned char* st = sm.stage[stage];
+    if (k == 0) {
+      // v rows of the tile -> vs (rows beyond the staged width read as zero)
+      named_bar_sync(1, GROUP_THREADS);  // previous unit's readers of vs are done
+      const float* Vs = reinterpret_cast<const float*>(st + K2_V);
+      for (int idx = ct; idx < NT * rows; idx += GROUP_THREADS) {
+        const int t = idx / rows, r = idx - t * rows;
+        vs[t * kMaxRank + r] = r < m.vrow ? Vs[t * m.vrow + r] : 0.f;
+      }
+      if (active && h == 0) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) Elem<T>::unpack(lds128(st + K2_Y + t * NC_BYTES + q * 16), yv[t]);
+      }
+      named_bar_sync(1, GROUP_THREADS);
+    }
+    if (active) {
+      // two pages per stage: thread h takes page pg0+h; a single page is split in row halves
+      const int nrow = m.npg == 2 ? kRowsPerPage : kRowsPerPage / 2;
+      const int r0 = m.npg == 2 ? 0 : h * (kRowsPerPage / 2);
+      const int pgl = m.npg == 2 ? h : 0;
+      const unsigned char* Bg = st + pgl * B_PITCH;
+      const int vbase = (m.pg0 + pgl) * kRowsPerPage;
+      for (int j = r0; j < r0 + nrow; ++j) {
+        float2 bf[NP2];
+        Elem<T>::unpack2(lds128(Bg + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const float vv = vs[t * kMaxRank + vbase + j];
+          const float2 v2 = make_float2(vv, vv);
+#pragma unroll
+          for (int e = 0; e < NP2; ++e) acc[t][e] = __ffma2_rn(v2, bf[e], acc[t][e]);
+        }
+      }
+    }
+    if (ct == 0) trace_consumer(p, seq, 3);
+    mbar_arrive(&sm.empty[stage]);
+  }
+  // combine the two halves (adjacent lanes), add into y, store
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int e = 0; e < NP2; ++e) {
+      acc[t][e].x += __shfl_xor_sync(0xffffffffu, acc[t][e].x, 1);
+      acc[t][e].y += __shfl_xor_sync(0xffffffffu, acc[t][e].y, 1);
+    }
+  if (active && h == 0) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+#pragma unroll
+      for (int e = 0; e < NP2; ++e) {
+        yv[t][2 * e] += acc[t][e].x;
+        yv[t][2 * e + 1] += acc[t][e].y;
+      }
+      char* dst = p.jobs[m0.job].y + ((long long)m0.rows[t] * p.h_out + m0.col0) * ES + q * 16;
+      *reinterpret_cast<uint4*>(dst) = Elem<T>::pack(yv[t]);
     }
   }
 }
 
-// =========================================================================== K2: expand
 template <typename T>
 __global__ void __launch_bounds__(NTHREADS, 1) lora_expand_kernel(const __grid_constant__ Params p) {
   constexpr int ES = Elem<T>::kBytes;
-  constexpr int EPV = Elem<T>::kEPV;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   K2Shared& sm = *reinterpret_cast<K2Shared*>(smem_raw);
   Plan& pl = sm.plan;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int S;
-  if (!prologue(p, sm, S) || !build_plan<T>(p, pl, S)) {
+  if (!prologue(p, sm, S)) {
     abort_launch(p);
     return;
   }
-  const int EX = pl.totals[1];
+  const int ncc = n_colchunks<T>(p);
+  const int UE = pl.totals[1] * ncc;
+  const int NW = pl.totals[5];
   const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
   const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
-  const int total = p.n_jobs * EX;
-  const int nkc = p.v_in ? 1 : ceil_div(p.h_in * ES, ACT_ROW_BYTES);
+  const int total = p.n_jobs * UE;
+  const int ncol_unit = NC_BYTES / ES;
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
-    const uint64_t pol_stream = policy_evict_first();
-    // this CTA's share of the expand work, balanced by bytes (rank-8 items carry half)
-    const long long cost_job = pl.totals[4];
-    auto item_at_cost = [&](long long c) -> int {
-      if (cost_job == 0) return 0;
-      const int jb = (int)(c / cost_job);
-      if (jb >= p.n_jobs) return total;
-      const int rem = (int)(c - jb * cost_job);
-      const int sg = seg_search(pl.ex_cost_start, S, rem);
-      int np_s, dummy1, dummy2, unit;
-      plan_counts<T>(p, pl.seg_off[sg + 1] - pl.seg_off[sg], pl.seg_sr[sg] & 511, dummy1, np_s, unit);
-      (void)dummy2;
-      const int local = unit > 0 ? ceil_div(rem - pl.ex_cost_start[sg], unit) : 0;
-      return jb * EX + pl.ex_start[sg] + min(local, np_s);
-    };
-    const long long cost_all = cost_job * p.n_jobs;
-    const int i0 = item_at_cost(cost_all * blockIdx.x / gridDim.x);
-    const int i1 = blockIdx.x + 1 == gridDim.x ? total : item_at_cost(cost_all * (blockIdx.x + 1) / gridDim.x);
-    int job = 0, s = 0, tile = 0, cc = 0;
-    int o0 = 0, Ts = 0, slot = 0, np = 0, nt = 0, p2 = 1, nq = 0, nc = 0, nexp = 0;
-    auto load_seg = [&]() {
-      o0 = pl.seg_off[s];
-      Ts = pl.seg_off[s + 1] - o0;
-      slot = pl.seg_sr[s] >> 9;
-      np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
-      nt = ceil_div(Ts, TG);
-      p2 = expand_p2(np);
-      nq = expand_nq(p2);
-      nc = nq * EPV;
-      nexp = ceil_div(p.h_out, nc);
-    };
-    if (i0 < i1) {
-      const ItemPos ip = locate(pl.ex_start, EX, S, i0);
-      job = ip.job;
-      s = ip.s;
-      load_seg();
-      tile = ip.local / nexp;
-      cc = ip.local - tile * nexp;
-    }
+    const uint64_t pol_w = policy_evict_first();
     bool waited = false;
     int seq = 0;
-    for (int item = i0; item < i1; ++item, ++seq) {
-      const unsigned long long t_it = p.trace ? gtimer() : 0;
-      const int stage = seq % NSTAGE;
-      const int col0 = cc * nc;
-      const int ncols = min(nc, p.h_out - col0);
-      const int pos0 = o0 + tile * TG;
-      const int tcount = min(TG, Ts - tile * TG);
+    int next = 0;
+    if (lane == 0) next = atomicAdd(p.ctr, 1);
+    for (;;) {
+      const int unit = __shfl_sync(0xffffffffu, next, 0);
+      if (unit >= total) break;
+      if (lane == 0) next = atomicAdd(p.ctr, 1);
+      const int job = unit / UE;
+      const int rem = unit - job * UE;
+      const int tl = rem / ncc;  // tile index in LPT order
+      const int oi = seg_search(pl.ex_start, NW, tl);
+      const int local = rem - pl.ex_start[oi] * ncc;
+      const int s = pl.order[oi];
+      const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
+      const int slot = pl.seg_sr[s] >> 9;
+      const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+      const int tile = local / ncc, cc = local - tile * ncc;
+      const int col0 = cc * ncol_unit;
+      const int ncols = min(ncol_unit, p.h_out - col0);
       const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
       const uint32_t y_bytes = ncols * ES;                  // per token
-      const int vrow = p.v_in ? min(np * kRowsPerPage, p.v_stride) : np * kRowsPerPage;  // floats per v row
-      const uint32_t v_row_bytes = vrow * 4;
-      const int nv = tcount * nkc;  // v rows staged
-      const bool v_staged = nv * (int)v_row_bytes <= V_BYTES;
+      const int pos0 = o0 + tile * TG;
+      const int tcount = min(TG, Ts - tile * TG);
+      const int rpad = np * kRowsPerPage;
+      const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
+      const int nst = ceil_div(np, PG);
       const Job& jb = p.jobs[job];
-      unsigned char* st = sm.stage[stage];
       int row = 0;
       if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
-      if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
-      const unsigned long long t_ready = p.trace ? gtimer() : 0;
-      __syncwarp();
-      Meta& m = sm.meta[stage];
-      if (lane == 0) {
-        m.kind = KIND_EXPAND; m.job = job; m.pos0 = pos0; m.T = tcount; m.np = np; m.col0 = col0;
-        m.ncols = ncols; m.nq = nq; m.p2 = p2; m.vrow = v_staged ? vrow : -vrow;
-        mbar_arrive_expect_tx(&sm.full[stage], b_bytes * np + y_bytes * tcount + (v_staged ? nv * v_row_bytes : 0));
-      }
-      if (lane < tcount) m.rows[lane] = row;
-      // weights and y rows do not depend on the shrink kernel: issue them first
-      for (int c = lane; c < np; c += 32) {
-        const int pgc = page_of(p, pl, pages_smem, s, slot, c);
-        const char* src = p.base + (long long)pgc * p.page_bytes + jb.b_off +
-                          (long long)(col0 * ES / kRowBytes) * kAtomBytes;
-        bulk_g2s(st + c * (nq * kRowBytes + PAGE_PAD), src, b_bytes, &sm.full[stage], pol_stream);
-      }
-      if (lane < tcount)
-        bulk_g2s(st + K2_B_REGION + lane * Y_ROW_BYTES, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes,
-                 &sm.full[stage], pol_stream);
-      if (!waited) {  // v is produced by the shrink kernel
-        pdl_wait();
-        pdl_launch_dependents();
-        waited = true;
-      }
-      if (v_staged) {
-        for (int c = lane; c < nv; c += 32) {
-          const int t = c / nkc, k2 = c - t * nkc;
-          const float* src = p.v_in ? p.v_in + (long long)(pos0 + t) * p.v_stride
-                                    : p.vws + (((long long)job * p.max_tokens + pos0 + t) * p.vws_kc + k2) * kMaxRank;
-          bulk_g2s(st + K2_B_REGION + TG * Y_ROW_BYTES + c * v_row_bytes, src, v_row_bytes, &sm.full[stage],
-                   pol_stream);
+      for (int k = 0; k < nst; ++k, ++seq) {
+        const unsigned long long t_it = p.trace ? gtimer() : 0;
+        const int stage = seq % NSTAGE;
+        const int pg0 = k * PG;
+        const int npg = min(PG, np - pg0);
+        unsigned char* st = sm.stage[stage];
+        uint32_t bytes = b_bytes * npg;
+        if (k == 0) bytes += y_bytes * tcount + tcount * vrow * 4;
+        if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+        const unsigned long long t_ready = p.trace ? gtimer() : 0;
+        __syncwarp();
+        Meta& m = sm.meta[stage];
+        if (lane == 0) {
+          m.kind = KIND_WORK; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+          m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
+          mbar_arrive_expect_tx(&sm.full[stage], bytes);
         }
-      }
-      if (p.trace && lane == 0 && seq < p.trace_cap) {
-        unsigned long long* tr = p.trace + ((long long)blockIdx.x * p.trace_cap + seq) * 8;
-        tr[0] = gtimer();
-        tr[1] = (2ull << 32) | (b_bytes * np + y_bytes * tcount + (v_staged ? nv * v_row_bytes : 0));
-        tr[4] = t_it;
-        tr[5] = t_ready;
-      }
-      // advance (column chunk fastest, then tile, segment, job)
-      if (++cc == nexp) {
-        cc = 0;
-        if (++tile == nt) {
-          tile = 0;
-          do {
-            if (++s == S) { s = 0; ++job; }
-          } while (job < p.n_jobs && pl.ex_start[s + 1] == pl.ex_start[s]);
-          if (job < p.n_jobs) load_seg();
+        if (lane < tcount) m.rows[lane] = row;
+        // B pages of this stage (weights: no dependency on the shrink kernel)
+        if (lane < npg) {
+          const int pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
+          const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
+          bulk_g2s(st + lane * B_PITCH, src, b_bytes, &sm.full[stage], pol_w);
         }
+        if (k == 0) {
+          if (lane < tcount)
+            bulk_g2s(st + K2_Y + lane * NC_BYTES, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes,
+                     &sm.full[stage], pol_w);
+          if (!waited) {  // v is produced by the shrink kernel
+            pdl_wait();
+            pdl_launch_dependents();
+            waited = true;
+          }
+          if (p.v_in) {
+            if (lane < tcount)
+              bulk_g2s(st + K2_V + lane * vrow * 4, p.v_in + (long long)(pos0 + lane) * p.v_stride, vrow * 4,
+                       &sm.full[stage], pol_w);
+          } else if (lane == 0) {
+            const float* src = p.vws + job * p.vws_job_stride + pl.v_start[s] + (long long)(tile * TG) * rpad;
+            bulk_g2s(st + K2_V, src, tcount * rpad * 4, &sm.full[stage], pol_w);
+          }
+        }
+        if (lane == 0) trace_producer(p, seq, t_it, t_ready, 2, bytes);
+        __syncwarp();
       }
-      __syncwarp();
     }
     if (!waited) pdl_wait();
     if (lane == 0) post_end(sm, seq);
   } else {
     // ------------------------------------------------------------------ consumers
-    const int grp = (warp - 1) / GROUP_WARPS;
-    const int ct = tid - 32 - grp * GROUP_THREADS;
-    const int bar_id = 1 + grp;
-    float* vs = reinterpret_cast<float*>(sm.scratch[grp]);  // [TG][kMaxRank]
-    for (int seq = grp;; seq += NGROUP) {
+    const int ct = tid - 32;
+    int seq = 0;
+    for (;;) {
       const int stage = seq % NSTAGE;
       mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
-      const Meta m = sm.meta[stage];
-      if (m.kind == KIND_END) break;
-      if (p.trace && ct == 0 && seq < p.trace_cap)
-        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 2] = gtimer();
-      const unsigned char* st = sm.stage[stage];
-      switch (m.T) {
-        case 1: expand_item<T, 1>(p, m, st, vs, nkc, ct, bar_id); break;
-        case 2: expand_item<T, 2>(p, m, st, vs, nkc, ct, bar_id); break;
-        case 3: expand_item<T, 3>(p, m, st, vs, nkc, ct, bar_id); break;
-        default: expand_item<T, 4>(p, m, st, vs, nkc, ct, bar_id); break;
+      const Meta m0 = sm.meta[stage];
+      if (m0.kind == KIND_END) break;
+      switch (m0.T) {
+        case 1: expand_unit<T, 1>(p, sm, seq, m0, ct); break;
+        case 2: expand_unit<T, 2>(p, sm, seq, m0, ct); break;
+        case 3: expand_unit<T, 3>(p, sm, seq, m0, ct); break;
+        default: expand_unit<T, 4>(p, sm, seq, m0, ct); break;
       }
-      if (p.trace && ct == 0 && seq < p.trace_cap)
-        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 3] = gtimer();
-      mbar_arrive(&sm.empty[stage]);
     }
   }
+  reset_counter_if_last(p);
 }
 
-// TP shrink: fold the k-chunk partials of every grouped position into v_out [pos][v_stride].
-__global__ void fold_partials_kernel(const float* __restrict__ vws, int vws_kc, int nkc,
-                                     const int* __restrict__ seg_off, const int* __restrict__ seg_slot,
-                                     const int* __restrict__ seg_rank, int n_seg, const int* __restrict__ n_seg_dev,
-                                     float* __restrict__ v_out, int v_stride) {
-  const int S = n_seg >= 0 ? n_seg : *n_seg_dev;
-  for (int s = blockIdx.x; s < S; s += gridDim.x) {
-    const int slot = seg_slot[s];
-    const int rows = slot >= 0 ? min(ceil_div(min(seg_rank[s], kMaxRank), kRowsPerPage) * kRowsPerPage, v_stride) : 0;
-    const int o0 = seg_off[s], o1 = seg_off[s + 1];
-    for (int idx = threadIdx.x; idx < (o1 - o0) * rows; idx += blockDim.x) {
-      const int t = idx / rows, r = idx - t * rows;
-      const float* src = vws + ((long long)(o0 + t) * vws_kc) * kMaxRank + r;
-      float sum = 0.f;
-      for (int k = 0; k < nkc; ++k) sum += src[k * kMaxRank];
-      v_out[(long long)(o0 + t) * v_stride + r] = sum;
+// One CTA builds the step's plan and writes it to global memory (consumed by every
+// lora_apply of the step through Params::plan).
+__global__ void __launch_bounds__(NTHREADS, 1) build_plan_kernel(const __grid_constant__ Params p, Plan* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Plan& pl = *reinterpret_cast<Plan*>(smem_raw);
+  const int S = p.n_seg >= 0 ? p.n_seg : *p.n_seg_dev;
+  bool ok = S >= 0 && S <= PLAN_SEGS;
+  if (ok) ok = build_plan(p, pl, S);
+  __syncthreads();
+  if (!ok) {
+    if (threadIdx.x == 0) {
+      *p.err = CHAM_ERR_LIMIT;
+      out->totals[2] = 1 << 30;  // consumers of this plan will refuse it
     }
+    return;
   }
+  const int4* src = reinterpret_cast<const int4*>(&pl);
+  int4* dst = reinterpret_cast<int4*>(out);
+  for (int i = threadIdx.x; i < (int)(sizeof(Plan) / 16); i += NTHREADS) dst[i] = src[i];
 }
 
 template <typename KernelT>
@@ -816,7 +797,7 @@ int launch_pdl(KernelT kern, int smem, const cham_pool* pool, const Params& prm,
 }
 
 template <typename T>
-int launch(cham_pool* pool, Params& prm, int mode, float* v_out, int v_stride, cudaStream_t stream) {
+int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
   static bool attr_set[2] = {false, false};
   auto k1 = lora_shrink_kernel<T>;
   auto k2 = lora_expand_kernel<T>;
@@ -827,9 +808,9 @@ int launch(cham_pool* pool, Params& prm, int mode, float* v_out, int v_stride, c
     attr_set[Elem<T>::kDtype] = true;
   }
   // ping-pong v workspace: apply n uses buffer n % 2 (see the ordering argument above)
-  const size_t buf_floats = (size_t)kMaxJobs * pool->max_tokens * pool->vws_kc * kMaxRank;
   Params p1 = prm;
-  p1.vws = pool->d_vws + (pool->apply_count & 1) * buf_floats;
+  p1.vws_job_stride = (long long)pool->max_tokens * kMaxRank;
+  p1.vws = pool->d_vws + (pool->apply_count & 1) * (size_t)kMaxJobs * p1.vws_job_stride;
   p1.ctr = pool->d_ctr;
   p1.err = pool->d_ctr + 2;
   Params p2 = p1;
@@ -838,14 +819,7 @@ int launch(cham_pool* pool, Params& prm, int mode, float* v_out, int v_stride, c
   ++pool->apply_count;
   if (mode != MODE_EXPAND) {
     int rc = launch_pdl(k1, s1, pool, p1, stream);
-    if (rc) return rc;
-  }
-  if (mode == MODE_SHRINK) {
-    fold_partials_kernel<<<pool->sm_count, 256, 0, stream>>>(
-        p1.vws, p1.vws_kc, ceil_div(prm.h_in * (int)sizeof(T), ACT_ROW_BYTES), prm.seg_off, prm.seg_slot,
-        prm.seg_rank, prm.n_seg, prm.n_seg_dev, v_out, v_stride);
-    CHAM_CUDA(cudaGetLastError());
-    return CHAM_OK;
+    if (rc || mode == MODE_SHRINK) return rc;
   }
   return launch_pdl(k2, s2, pool, p2, stream);
 }
@@ -855,7 +829,7 @@ int launch(cham_pool* pool, Params& prm, int mode, float* v_out, int v_stride, c
 // Shared validation + parameter setup for the four entry points.
 int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
                  void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
-                 const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream, int mode,
+                 const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream, int mode,
                  float* v_out, const float* v_in, int v_stride) {
   using namespace decode;
   if (!pool) return fail(CHAM_ERR_INVALID, "lora_apply: null pool");
@@ -868,7 +842,8 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   if (n_tokens < 0 || n_tokens > pool->max_tokens)
     return fail(CHAM_ERR_LIMIT, "lora_apply: n_tokens exceeds the pool's max_tokens");
   if (mode != MODE_FUSED && n_jobs != 1) return fail(CHAM_ERR_INVALID, "shrink/expand take one projection");
-  if (v_in && (v_stride % 4)) return fail(CHAM_ERR_INVALID, "lora_expand: v_stride must be a multiple of 4");
+  if ((v_in || v_out) && (v_stride <= 0 || v_stride % 4))
+    return fail(CHAM_ERR_INVALID, "lora_shrink/expand: v_stride must be a positive multiple of 4");
   Params prm{};
   prm.base = pool->base;
   prm.page_bytes = (long long)pool->page_bytes;
@@ -899,15 +874,41 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   prm.seg_rank = seg_rank;
   prm.n_seg = n_seg;
   prm.n_seg_dev = n_seg_dev;
-  prm.vws_kc = pool->vws_kc;
   prm.max_tokens = pool->max_tokens;
-  prm.v_in = v_in;
+  prm.v_out = mode == MODE_SHRINK ? v_out : nullptr;
+  prm.v_in = mode == MODE_EXPAND ? v_in : nullptr;
   prm.v_stride = v_stride;
   prm.trace = pool->d_trace;
   prm.trace_cap = pool->trace_cap;
-  if (pool->dtype == CHAM_BF16)
-    return launch<__nv_bfloat16>(pool, prm, mode, v_out, v_stride, (cudaStream_t)stream);
-  return launch<float>(pool, prm, mode, v_out, v_stride, (cudaStream_t)stream);
+  prm.plan = plan;
+  if (pool->dtype == CHAM_BF16) return launch<__nv_bfloat16>(pool, prm, mode, (cudaStream_t)stream);
+  return launch<float>(pool, prm, mode, (cudaStream_t)stream);
 }
 
+}  // namespace cham
+
+namespace cham {
+size_t plan_bytes() { return sizeof(decode::Plan); }
+
+int build_plan_entry(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
+                     const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan, void* stream) {
+  using namespace decode;
+  if (!pool || !plan || !seg_off || !seg_slot || !seg_rank) return fail(CHAM_ERR_INVALID, "cham_build_plan: null argument");
+  if (n_seg < 0 && !n_seg_dev) return fail(CHAM_ERR_INVALID, "cham_build_plan: n_seg < 0 needs n_seg_dev");
+  if (n_seg > PLAN_SEGS) return fail(CHAM_ERR_LIMIT, "cham_build_plan: too many segments");
+  if (reinterpret_cast<uintptr_t>(plan) & 15) return fail(CHAM_ERR_INVALID, "cham_build_plan: plan must be 16-byte aligned");
+  Params prm{};
+  prm.slot_pages = pool->d_slot_pages;
+  prm.perm = perm;
+  prm.seg_off = seg_off;
+  prm.seg_slot = seg_slot;
+  prm.seg_rank = seg_rank;
+  prm.n_seg = n_seg;
+  prm.n_seg_dev = n_seg_dev;
+  prm.max_tokens = pool->max_tokens;
+  prm.err = pool->d_ctr + 2;
+  build_plan_kernel<<<1, NTHREADS, sizeof(Plan), (cudaStream_t)stream>>>(prm, static_cast<Plan*>(plan));
+  CHAM_CUDA(cudaGetLastError());
+  return CHAM_OK;
+}
 }  // namespace cham

@@ -178,7 +178,7 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   if (e == cudaSuccess) e = cudaMalloc(&pool->d_slot_rank, sizeof(int) * (size_t)n_slots);
   if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 8);
   if (e == cudaSuccess)
-    e = cudaMalloc(&pool->d_vws, 2 * sizeof(float) * (size_t)kMaxJobs * max_tokens * pool->vws_kc * kMaxRank);
+    e = cudaMalloc(&pool->d_vws, 2 * sizeof(float) * (size_t)kMaxJobs * max_tokens * kMaxRank);
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);

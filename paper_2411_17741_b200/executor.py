@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .ops import SegmentTable, build_segments, lora_apply_multi, lora_apply_table
+from .ops import SegmentTable, build_plan, build_segments, lora_apply_multi, lora_apply_table
 from .pool import AdapterPool
 
 
@@ -103,9 +103,11 @@ class LoraStepExecutor:
 
     # -- device side (capturable) ------------------------------------------------------------
     def build(self, stream=None) -> SegmentTable:
+        """K4 segment table + the step's launch plan (two single-CTA kernels)."""
         n = self.n_req
         build_segments(self.req_dev[0, :n], self.req_dev[1, :n], self.req_dev[2, :n], device=self.pool.device,
                        stream=stream, out=self.table)
+        build_plan(self.table, pool=self.pool, stream=stream)
         return self.table
 
     def apply_layer(self, layer: int, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], stream=None):
@@ -119,7 +121,8 @@ class LoraStepExecutor:
                                  layer=layer, projs=projs, stream=stream)
 
     def launches_per_step(self) -> int:
-        return 1 + self.pool.n_layers * len(self.proj_groups)
+        """Kernels per step: segment builder + plan + (shrink, expand) per (layer, group)."""
+        return 2 + 2 * self.pool.n_layers * len(self.proj_groups)
 
     def run(self, xs_per_layer, ys_per_layer, stream=None) -> None:
         """K4 + every (layer, group) apply, on `stream`."""

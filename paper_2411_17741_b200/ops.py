@@ -31,6 +31,7 @@ class SegmentTable:
     n_seg: torch.Tensor
     n_tokens: int
     n_seg_host: Optional[int] = None
+    plan: Optional[torch.Tensor] = None  # device launch plan (build_plan), valid for one step
 
     def to_host(self):
         """(perm, seg_off, seg_slot, seg_rank) trimmed to the real segment count, numpy."""
@@ -82,6 +83,21 @@ def build_segments(req_slot, req_rank, req_ntok, *, device=None, stream=None,
     return out
 
 
+def plan_bytes() -> int:
+    return int(_lib.lib().cham_plan_bytes())
+
+
+def build_plan(table: SegmentTable, *, pool: AdapterPool, stream=None) -> torch.Tensor:
+    """Device launch plan for `table` against the pool's slot table (one CTA).  Every
+    lora_apply of the step reuses it, so the kernels skip their own plan construction."""
+    if table.plan is None:
+        table.plan = torch.empty(plan_bytes(), dtype=torch.uint8, device=pool.device)
+    call("cham_build_plan", pool.handle, table.perm.data_ptr(), table.seg_off.data_ptr(), table.seg_slot.data_ptr(),
+         table.seg_rank.data_ptr(), -1 if table.n_seg_host is None else table.n_seg_host, table.n_seg.data_ptr(),
+         table.plan.data_ptr(), _stream_ptr(stream))
+    return table.plan
+
+
 def _check_act(t: torch.Tensor, pool: AdapterPool, cols: int, name: str) -> None:
     if t.device != pool.device:
         raise ValueError(f"{name} must live on {pool.device}")
@@ -98,7 +114,7 @@ def _tables(slot_ids, seg_offsets, ranks, perm, device):
 
 def lora_apply(x: torch.Tensor, y: torch.Tensor, slot_ids, seg_offsets, ranks, *, pool: AdapterPool,
                layer: int, proj: int, perm=None, n_seg: Optional[int] = None, n_seg_dev=None,
-               stream=None) -> torch.Tensor:
+               plan: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """y[t] += (x[t] . A_slot) . B_slot for every token of every segment (in place).
 
     x: [T, h_in[proj]], y: [T, h_out[proj]] in the pool dtype on the pool device.
@@ -116,7 +132,7 @@ def lora_apply(x: torch.Tensor, y: torch.Tensor, slot_ids, seg_offsets, ranks, *
         n_seg = ss.numel()
     call("cham_lora_apply", pool.handle, int(layer), int(proj), x.data_ptr(), y.data_ptr(), int(x.shape[0]),
          _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(), -1 if n_seg is None else int(n_seg),
-         _lib.ptr(n_seg_dev), _stream_ptr(stream))
+         _lib.ptr(n_seg_dev), _lib.ptr(plan), _stream_ptr(stream))
     return y
 
 
@@ -126,7 +142,8 @@ def lora_apply_table(x, y, table: SegmentTable, *, pool: AdapterPool, layer: int
     _check_act(y, pool, pool.h_out[proj], "y")
     call("cham_lora_apply", pool.handle, int(layer), int(proj), x.data_ptr(), y.data_ptr(), int(x.shape[0]),
          table.perm.data_ptr(), table.seg_off.data_ptr(), table.seg_slot.data_ptr(), table.seg_rank.data_ptr(),
-         -1 if table.n_seg_host is None else table.n_seg_host, table.n_seg.data_ptr(), _stream_ptr(stream))
+         -1 if table.n_seg_host is None else table.n_seg_host, table.n_seg.data_ptr(), _lib.ptr(table.plan),
+         _stream_ptr(stream))
     return y
 
 
@@ -143,11 +160,13 @@ def lora_apply_multi(xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], tab
     ya = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
     call("cham_lora_apply_multi", pool.handle, int(layer), n, _lib.int_array(projs), xa, ya, int(xs[0].shape[0]),
          table.perm.data_ptr(), table.seg_off.data_ptr(), table.seg_slot.data_ptr(), table.seg_rank.data_ptr(),
-         -1 if table.n_seg_host is None else table.n_seg_host, table.n_seg.data_ptr(), _stream_ptr(stream))
+         -1 if table.n_seg_host is None else table.n_seg_host, table.n_seg.data_ptr(), _lib.ptr(table.plan),
+         _stream_ptr(stream))
 
 
 def lora_shrink(x: torch.Tensor, v: torch.Tensor, slot_ids, seg_offsets, ranks, *, pool: AdapterPool,
-                layer: int, proj: int, perm=None, n_seg: Optional[int] = None, stream=None) -> torch.Tensor:
+                layer: int, proj: int, perm=None, n_seg: Optional[int] = None, plan=None,
+                stream=None) -> torch.Tensor:
     """v[k, :r] = x[perm[k]] . A_slot (fp32 [n_positions, v_stride]); the TP all-reduce operand."""
     _check_act(x, pool, pool.h_in[proj], "x")
     if v.dtype != torch.float32 or v.dim() != 2 or not v.is_contiguous():
@@ -155,12 +174,13 @@ def lora_shrink(x: torch.Tensor, v: torch.Tensor, slot_ids, seg_offsets, ranks, 
     ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
     call("cham_lora_shrink", pool.handle, int(layer), int(proj), x.data_ptr(), v.data_ptr(), int(v.shape[1]),
          int(x.shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
-         ss.numel() if n_seg is None else int(n_seg), None, _stream_ptr(stream))
+         ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))
     return v
 
 
 def lora_expand(v: torch.Tensor, y: torch.Tensor, slot_ids, seg_offsets, ranks, *, pool: AdapterPool,
-                layer: int, proj: int, perm=None, n_seg: Optional[int] = None, stream=None) -> torch.Tensor:
+                layer: int, proj: int, perm=None, n_seg: Optional[int] = None, plan=None,
+                stream=None) -> torch.Tensor:
     """y[perm[k]] += v[k, :r] . B_slot (in place)."""
     _check_act(y, pool, pool.h_out[proj], "y")
     if v.dtype != torch.float32 or v.dim() != 2 or not v.is_contiguous():
@@ -168,5 +188,5 @@ def lora_expand(v: torch.Tensor, y: torch.Tensor, slot_ids, seg_offsets, ranks, 
     ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
     call("cham_lora_expand", pool.handle, int(layer), int(proj), v.data_ptr(), int(v.shape[1]), y.data_ptr(),
          int(y.shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
-         ss.numel() if n_seg is None else int(n_seg), None, _stream_ptr(stream))
+         ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))
     return y

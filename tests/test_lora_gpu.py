@@ -196,3 +196,42 @@ def test_device_segment_builder_bit_exact():
         want = build_segments_ref(slots, ranks, ntok)
         for g, w in zip(got, want):
             np.testing.assert_array_equal(g, w)
+
+
+def test_prebuilt_plan_matches_in_kernel_plan():
+    """The step-level plan (cham_build_plan) gives bit-identical results to the kernels'
+    own plan construction, including multi-projection launches."""
+    from paper_2411_17741_b200.ops import build_plan, build_segments, lora_apply_multi, lora_apply_table
+
+    rng = np.random.default_rng(8)
+    slot_ranks = {0: 8, 1: 16, 2: 32, 3: 64, 4: 128}
+    adapters = make_adapters(rng, slot_ranks, 4096, 4096, bf16=True)
+    pool = _pool(1, [4096] * 3, [4096] * 3, torch.bfloat16, 2 * sum(-(-r // 8) for r in slot_ranks.values()))
+    page = 0
+    for s, r in slot_ranks.items():
+        n = -(-r // 8)
+        pool.set_slot(s, r, list(range(page, page + n)))
+        page += n
+        a, b = adapters[s]
+        at, bt = torch.from_numpy(a), torch.from_numpy(b)
+        pool.fill_async(s, pool.pack_host([at, at * 0.5, at * 2], [bt, bt, bt * 0.25], r))
+    torch.cuda.synchronize()
+    slots = rng.integers(0, 5, 200)
+    ntok = rng.integers(1, 4, 200)
+    tbl = build_segments(slots, [slot_ranks[int(s)] for s in slots], ntok)
+    T = int(ntok.sum())
+    x = torch.from_numpy(bf16_round(rng.standard_normal((T, 4096)).astype(np.float32))).cuda().to(torch.bfloat16)
+    ys0 = [torch.from_numpy(bf16_round(rng.standard_normal((T, 4096)).astype(np.float32))).cuda().to(torch.bfloat16)
+           for _ in range(3)]
+    ya = [y.clone() for y in ys0]
+    lora_apply_multi([x] * 3, ya, tbl, pool=pool, layer=0, projs=[0, 1, 2])
+    yb = [y.clone() for y in ys0]
+    build_plan(tbl, pool=pool)
+    lora_apply_multi([x] * 3, yb, tbl, pool=pool, layer=0, projs=[0, 1, 2])
+    yc = ys0[1].clone()
+    lora_apply_table(x, yc, tbl, pool=pool, layer=0, proj=1)
+    torch.cuda.synchronize()
+    for a_, b_ in zip(ya, yb):
+        assert torch.equal(a_, b_)
+    assert torch.equal(yb[1], yc)
+    pool.close()
