@@ -1,6 +1,7 @@
-// cham_decode.cu — K1 (segmented shrink, h_in -> r) and K2 (segmented expand, r -> h_out,
-// accumulated into y) for decode-sized segments: two persistent, warp-specialised kernels
-// chained with programmatic dependent launch (PDL).
+// cham_decode.cu — segmented shrink (h_in -> r) and expand (r -> h_out, accumulated into y)
+// for decode-sized segments: ONE persistent, warp-specialised kernel per lora_apply with two
+// phases separated by a grid barrier; consecutive applies overlap through programmatic
+// dependent launch (PDL).
 //
 // Reference seam: CostModel.step_duration's LoRA term (engine.py:67-77) models
 //   adapter_units = sum_decoders rank + sum_prefills rank * input_tokens
@@ -18,12 +19,15 @@
 //  * Units are taken dynamically from a global counter (the next index is prefetched while
 //    the current unit streams).  K2 walks segments largest-rank first (LPT), so the tail
 //    is made of the small rank-8 units.
-//  * Warp 0 produces (plan in shared memory: no L2 round trips in the loop), 8 consumer
+//  * Warp 8 produces (plan in shared memory: no L2 round trips in the loop), 8 consumer
 //    warps compute with packed FFMA2 (fp32 accumulate).  Weights are issued before
-//    griddepcontrol.wait, activations / v after it; K2's dependency on K1 is the kernel
-//    boundary — no fences, flags or spin-waits inside a kernel.  Every CTA executes
-//    griddepcontrol.wait before exiting, so kernel n completes after kernel n-1 and the
-//    ping-pong v buffer of apply n-2 is free when apply n writes it.
+//    griddepcontrol.wait, activations after it.  Between the phases the producer posts a
+//    marker stage; on it the consumers publish their v rows (release) and arrive at a
+//    sense-reversal grid barrier, while the producer already streams phase-2 B pages and
+//    y rows; only the v copies wait for the barrier (acquire + async-proxy fence).  The
+//    grid is one CTA per SM (co-resident).  Every CTA executes griddepcontrol.wait before
+//    exiting, so apply n completes after apply n-1 and the ping-pong v buffer of apply
+//    n-2 is free when apply n writes it.
 #include "cham_pool.h"
 
 namespace cham {
@@ -53,7 +57,7 @@ constexpr int PLAN_TOKENS = 2048;
 static_assert(PLAN_SEGS == kMaxSegments, "limits");
 
 enum Mode { MODE_FUSED = 0, MODE_SHRINK = 1, MODE_EXPAND = 2 };
-enum Kind { KIND_END = 0, KIND_WORK = 1 };
+enum Kind { KIND_END = 0, KIND_SHRINK = 1, KIND_EXPAND = 2, KIND_PHASE = 3 };
 
 struct Job {
   const char* x;
@@ -75,7 +79,8 @@ struct Params {
   const int* seg_rank;
   int n_seg;
   const int* n_seg_dev;
-  int* ctr;        // [0] next unit, [1] finished CTAs
+  int* ctr;        // [0] next shrink unit, [1] finished CTAs, [4] next expand unit,
+                   // [8] grid-barrier arrivals, [9] grid-barrier generation
   int* err;
   float* vws;      // this apply's compact v buffer: [job][sum_s T_s * rpad_s]
   long long vws_job_stride;
@@ -120,7 +125,8 @@ struct alignas(16) Plan {
 };
 static_assert(sizeof(Plan) % 16 == 0, "the plan is moved with one bulk copy");
 
-template <int STAGE_BYTES, int SCRATCH_BYTES>
+constexpr int STAGE_BYTES = K1_STAGE > K2_STAGE ? K1_STAGE : K2_STAGE;
+constexpr int SCRATCH_BYTES = TG * kMaxRank * 4;  // K2 v rows; K1 uses the first 1 KiB
 struct Shared {
   alignas(128) unsigned char stage[NSTAGE][STAGE_BYTES];
   alignas(16) unsigned char scratch[SCRATCH_BYTES];
@@ -128,10 +134,12 @@ struct Shared {
   uint64_t empty[NSTAGE];
   Meta meta[NSTAGE];
   uint64_t plan_bar;
+  int grid_gen;  // grid-barrier generation observed at kernel start
+  int unit_mailbox;
   Plan plan;
 };
-using K1Shared = Shared<K1_STAGE, GROUP_WARPS * 32 * 4>;
-using K2Shared = Shared<K2_STAGE, TG * kMaxRank * 4>;
+using K1Shared = Shared;
+using K2Shared = Shared;
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ constexpr int cpow2(int v) { return v <= 1 ? 1 : 2 * cpow2((v + 1) / 2); }
@@ -316,26 +324,7 @@ __device__ __forceinline__ int row_of(const Params& p, const Plan& pl, bool perm
   return perm_smem ? (int)pl.perm[pos] : (p.perm ? __ldg(p.perm + pos) : pos);
 }
 
-template <class SH>
-__device__ __forceinline__ void post_end(SH& sm, int seq) {
-  const int st = seq % NSTAGE;
-  mbar_wait(&sm.empty[st], ((seq / NSTAGE) & 1) ^ 1);
-  sm.meta[st].kind = KIND_END;
-  mbar_arrive(&sm.full[st]);
-}
 
-// The last CTA to finish re-arms the unit counter for the next launch of this kernel.
-__device__ __forceinline__ void reset_counter_if_last(const Params& p) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
-      p.ctr[0] = 0;
-      p.ctr[1] = 0;
-      __threadfence();
-    }
-  }
-}
 
 // Barriers + plan.  A prebuilt plan is pulled into shared memory with one bulk copy (the
 // plan is written by an earlier kernel of the step, so it may be read before the PDL wait).
@@ -454,107 +443,6 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(NTHREADS, 1) lora_shrink_kernel(const __grid_constant__ Params p) {
-  constexpr int ES = Elem<T>::kBytes;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  K1Shared& sm = *reinterpret_cast<K1Shared*>(smem_raw);
-  Plan& pl = sm.plan;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  int S;
-  if (!prologue(p, sm, S)) {
-    abort_launch(p);
-    return;
-  }
-  S = pl.n_seg;
-  const int US = pl.totals[0];
-  const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
-  const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
-  const int total = p.n_jobs * US;
-  const int nkc = n_kchunks<T>(p);
-  const int natoms = p.h_in * ES / kRowBytes;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------------ producer
-    const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
-    const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page of the tile
-    bool waited = false;
-    int seq = 0;
-    int next = 0;
-    if (lane == 0) next = atomicAdd(p.ctr, 1);
-    for (;;) {
-      const int unit = __shfl_sync(0xffffffffu, next, 0);
-      if (unit >= total) break;
-      if (lane == 0) next = atomicAdd(p.ctr, 1);  // prefetch the next unit index
-      const int job = unit / US;
-      const int rem = unit - job * US;
-      const int s = seg_search(pl.sh_start, S, rem);
-      const int local = rem - pl.sh_start[s];
-      const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
-      const int slot = pl.seg_sr[s] >> 9;
-      const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
-      const int tile = local / np, g = local - tile * np;
-      const int pos0 = o0 + tile * TG;
-      const int tcount = min(TG, Ts - tile * TG);
-      const Job& jb = p.jobs[job];
-      int row = 0;
-      if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
-      const int pg = page_of(p, pl, pages_smem, s, slot, g);
-      const char* a_src = p.base + (long long)pg * p.page_bytes + jb.a_off;
-      for (int kc = 0; kc < nkc; ++kc, ++seq) {
-        const unsigned long long t_it = p.trace ? gtimer() : 0;
-        const int stage = seq % NSTAGE;
-        const int a0 = kc * (A_CHUNK / kAtomBytes);
-        const uint32_t a_bytes = min(A_CHUNK / kAtomBytes, natoms - a0) * kAtomBytes;
-        const uint32_t x_bytes = a_bytes / kRowsPerPage;
-        unsigned char* st = sm.stage[stage];
-        if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
-        const unsigned long long t_ready = p.trace ? gtimer() : 0;
-        __syncwarp();
-        Meta& m = sm.meta[stage];
-        if (lane == 0) {
-          m.kind = KIND_WORK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
-          m.g = g; m.kc = kc;
-          mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
-          bulk_g2s(st, a_src + (long long)a0 * kAtomBytes, a_bytes, &sm.full[stage], pol_w);
-        }
-        if (lane < tcount) m.rows[lane] = row;
-        if (!waited) {  // x may be produced by the previous kernel
-          pdl_wait();
-          pdl_launch_dependents();
-          waited = true;
-        }
-        if (lane < tcount)
-          bulk_g2s(st + A_CHUNK + lane * X_ROW, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
-                   &sm.full[stage], pol_x);
-        if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
-        __syncwarp();
-      }
-    }
-    if (!waited) pdl_wait();
-    if (lane == 0) post_end(sm, seq);
-  } else {
-    // ------------------------------------------------------------------ consumers
-    const int ct = tid - 32;
-    const int gw = ct >> 5;
-    float* red = reinterpret_cast<float*>(sm.scratch);
-    int seq = 0;
-    for (;;) {
-      const int stage = seq % NSTAGE;
-      mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
-      const Meta m0 = sm.meta[stage];
-      if (m0.kind == KIND_END) break;
-      switch (m0.T) {
-        case 1: shrink_unit<T, 1>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
-        case 2: shrink_unit<T, 2>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
-        case 3: shrink_unit<T, 3>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
-        default: shrink_unit<T, 4>(p, pl, sm, seq, m0, red, ct, lane, gw); break;
-      }
-    }
-  }
-  reset_counter_if_last(p);
-}
-
 // =========================================================================== K2: expand
 // One unit: output tile [NT tokens x 1024 columns]; stages walk the adapter's pages two at
 // a time.  Thread (q, h) owns 16-byte column chunk q (= ct >> 1) and page / half-page h.
@@ -573,7 +461,6 @@ __device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& 
   for (int t = 0; t < NT; ++t)
 #pragma unroll
     for (int e = 0; e < NP2; ++e) acc[t][e] = make_float2(0.f, 0.f);
-  float yv[NT][EPV];  // this thread's share of the y rows (staged with the first stage)
   for (int k = 0; k < m0.nst; ++k, ++seq) {
     const int stage = seq % NSTAGE;
     if (k > 0) mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
@@ -587,10 +474,6 @@ __device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& 
       for (int idx = ct; idx < NT * rows; idx += GROUP_THREADS) {
         const int t = idx / rows, r = idx - t * rows;
         vs[t * kMaxRank + r] = r < m.vrow ? Vs[t * m.vrow + r] : 0.f;
-      }
-      if (active && h == 0) {
-#pragma unroll
-        for (int t = 0; t < NT; ++t) Elem<T>::unpack(lds128(st + K2_Y + t * NC_BYTES + q * 16), yv[t]);
       }
       named_bar_sync(1, GROUP_THREADS);
     }
@@ -613,43 +496,169 @@ __device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& 
         }
       }
     }
+    if (k == m0.nst - 1) {
+      // epilogue on the last stage (it carries the y rows): combine the two halves held
+      // by adjacent lanes, add into y, store
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < NP2; ++e) {
+          acc[t][e].x += __shfl_xor_sync(0xffffffffu, acc[t][e].x, 1);
+          acc[t][e].y += __shfl_xor_sync(0xffffffffu, acc[t][e].y, 1);
+        }
+      if (active) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          // lane h stores tokens t == h (mod 2)
+          if ((t & 1) == h) {
+            float yv[EPV];
+            Elem<T>::unpack(lds128(st + K2_Y + t * NC_BYTES + q * 16), yv);
+#pragma unroll
+            for (int e = 0; e < NP2; ++e) {
+              yv[2 * e] += acc[t][e].x;
+              yv[2 * e + 1] += acc[t][e].y;
+            }
+            char* dst = p.jobs[m0.job].y + ((long long)m0.rows[t] * p.h_out + m0.col0) * ES + q * 16;
+            *reinterpret_cast<uint4*>(dst) = Elem<T>::pack(yv);
+          }
+        }
+      }
+    }
     if (ct == 0) trace_consumer(p, seq, 3);
     mbar_arrive(&sm.empty[stage]);
   }
-  // combine the two halves (adjacent lanes), add into y, store
-#pragma unroll
-  for (int t = 0; t < NT; ++t)
-#pragma unroll
-    for (int e = 0; e < NP2; ++e) {
-      acc[t][e].x += __shfl_xor_sync(0xffffffffu, acc[t][e].x, 1);
-      acc[t][e].y += __shfl_xor_sync(0xffffffffu, acc[t][e].y, 1);
-    }
-  if (active && h == 0) {
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-#pragma unroll
-      for (int e = 0; e < NP2; ++e) {
-        yv[t][2 * e] += acc[t][e].x;
-        yv[t][2 * e + 1] += acc[t][e].y;
-      }
-      char* dst = p.jobs[m0.job].y + ((long long)m0.rows[t] * p.h_out + m0.col0) * ES + q * 16;
-      *reinterpret_cast<uint4*>(dst) = Elem<T>::pack(yv[t]);
-    }
-  }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(NTHREADS, 1) lora_expand_kernel(const __grid_constant__ Params p) {
-  constexpr int ES = Elem<T>::kBytes;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  K2Shared& sm = *reinterpret_cast<K2Shared*>(smem_raw);
-  Plan& pl = sm.plan;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  int S;
-  if (!prologue(p, sm, S)) {
-    abort_launch(p);
-    return;
+// =========================================================================== fused kernel
+// Dynamic unit dispatch for the producer warp: lanes [0, depth) each hold one outstanding
+// counter value (an atomicAdd issued depth-1 units earlier).  The raw atomic result is kept
+// untouched until the slot is consumed, so the warp never waits on the counter's L2 round
+// trip.  The first unit of every CTA is static.  Unit index = slot value + gridDim.x.
+// Plain (non-aggregated) fetch-and-increment (atom.inc cannot be warp-aggregated; the
+// aggregated atomicAdd reads its result with a shuffle at once = an L2 round-trip stall).
+__device__ __forceinline__ int atom_add_lazy(int* p) {
+  int old;
+  asm volatile("atom.global.inc.u32 %0, [%1], 2147483647;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
+struct UnitQueue {
+  int q;  // this lane's raw slot value (lanes < depth)
+  int head;
+  int depth;
+  int* ctr;
+  int total;
+  volatile int* xfer;  // shared-memory mailbox: only the head lane reads its own slot
+  __device__ __forceinline__ void init(int* c, int tot, int d, int lane, int* mailbox) {
+    ctr = c;
+    total = tot;
+    depth = d;
+    xfer = mailbox;
+    head = 0;
+    q = 1 << 29;
+    if (lane == 0) q = (int)blockIdx.x - (int)gridDim.x;
+    else if (lane < depth) q = atom_add_lazy(ctr);
   }
+  // next unit index for this CTA, or -1 when the unit space is exhausted
+  __device__ __forceinline__ int next(int lane) {
+    for (;;) {
+      // a shuffle would read q in every lane and wait on every outstanding atomic
+      if (lane == head) *xfer = q;
+      __syncwarp();
+      const int u = *xfer + (int)gridDim.x;
+      __syncwarp();
+      const int h = head;
+      head = head + 1 == depth ? 0 : head + 1;
+      if (u < total) {
+        if (lane == h) q = atom_add_lazy(ctr);  // refill; the result is read depth-1 units later
+        return u;
+      }
+      if (!__any_sync(0xffffffffu, lane < depth && q + (int)gridDim.x < total)) return -1;
+    }
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ int produce_shrink(const Params& p, Shared& sm, int seq, bool& waited) {
+  constexpr int ES = Elem<T>::kBytes;
+  const Plan& pl = sm.plan;
+  const int lane = threadIdx.x & 31;
+  const int S = pl.n_seg;
+  const int US = pl.totals[0];
+  const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
+  const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
+  const int total = p.n_jobs * US;
+  const int nkc = n_kchunks<T>(p);
+  const int natoms = p.h_in * ES / kRowBytes;
+  const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
+  const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page of the tile
+  UnitQueue uq;
+  uq.init(p.ctr, total, 3, lane, &sm.unit_mailbox);  // uniform units: prefetch two ahead
+  for (;;) {
+    const unsigned long long t_u0 = p.trace ? gtimer() : 0;
+    const int unit = uq.next(lane);
+    if (unit < 0) break;
+    const unsigned long long t_u1 = p.trace ? gtimer() : 0;
+    const int job = unit / US;
+    const int rem = unit - job * US;
+    const int s = seg_search(pl.sh_start, S, rem);
+    const int local = rem - pl.sh_start[s];
+    const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
+    const int slot = pl.seg_sr[s] >> 9;
+    const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+    const int tile = local / np, g = local - tile * np;
+    const int pos0 = o0 + tile * TG;
+    const int tcount = min(TG, Ts - tile * TG);
+    const Job& jb = p.jobs[job];
+    int row = 0;
+    if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
+    const int pg = page_of(p, pl, pages_smem, s, slot, g);
+    const char* a_src = p.base + (long long)pg * p.page_bytes + jb.a_off;
+    const unsigned long long t_u2 = p.trace ? gtimer() : 0;
+    if (p.trace && lane == 0 && seq < p.trace_cap) {
+      p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 6] = (t_u1 - t_u0);
+      p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 7] = (t_u2 - t_u1);
+    }
+    for (int kc = 0; kc < nkc; ++kc, ++seq) {
+      const unsigned long long t_it = p.trace ? gtimer() : 0;
+      const int stage = seq % NSTAGE;
+      const int a0 = kc * (A_CHUNK / kAtomBytes);
+      const uint32_t a_bytes = min(A_CHUNK / kAtomBytes, natoms - a0) * kAtomBytes;
+      const uint32_t x_bytes = a_bytes / kRowsPerPage;
+      unsigned char* st = sm.stage[stage];
+      if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+      const unsigned long long t_ready = p.trace ? gtimer() : 0;
+      __syncwarp();
+      Meta& m = sm.meta[stage];
+      if (lane == 0) {
+        m.kind = KIND_SHRINK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+        m.g = g; m.kc = kc;
+        mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
+        bulk_g2s(st, a_src + (long long)a0 * kAtomBytes, a_bytes, &sm.full[stage], pol_w);
+      }
+      if (lane < tcount) m.rows[lane] = row;
+      if (!waited) {  // x may be produced by the previous kernel
+        pdl_wait();
+        pdl_launch_dependents();
+        waited = true;
+      }
+      if (lane < tcount)
+        bulk_g2s(st + A_CHUNK + lane * X_ROW, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
+                 &sm.full[stage], pol_x);
+      if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
+      __syncwarp();
+    }
+  }
+  return seq;
+}
+
+// Producer side of phase 2 (expand units).  In fused mode the v copies wait for the grid
+// barrier (every CTA finished phase 1); B pages and y rows are prefetched before it.
+template <typename T>
+__device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused) {
+  constexpr int ES = Elem<T>::kBytes;
+  const Plan& pl = sm.plan;
+  const int lane = threadIdx.x & 31;
   const int ncc = n_colchunks<T>(p);
   const int UE = pl.totals[1] * ncc;
   const int NW = pl.totals[5];
@@ -657,106 +666,186 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_expand_kernel(const __grid_c
   const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
   const int total = p.n_jobs * UE;
   const int ncol_unit = NC_BYTES / ES;
+  const uint64_t pol_w = policy_evict_first();
+  bool v_ready = !fused;
+  UnitQueue uq;
+  uq.init(p.ctr + 4, total, 2, lane, &sm.unit_mailbox);  // variable units: one ahead keeps the LPT balance
+  for (;;) {
+    const int unit = uq.next(lane);
+    if (unit < 0) break;
+    const int job = unit / UE;
+    const int rem = unit - job * UE;
+    const int tl = rem / ncc;  // tile index in LPT order
+    const int oi = seg_search(pl.ex_start, NW, tl);
+    const int local = rem - pl.ex_start[oi] * ncc;
+    const int s = pl.order[oi];
+    const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
+    const int slot = pl.seg_sr[s] >> 9;
+    const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+    const int tile = local / ncc, cc = local - tile * ncc;
+    const int col0 = cc * ncol_unit;
+    const int ncols = min(ncol_unit, p.h_out - col0);
+    const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
+    const uint32_t y_bytes = ncols * ES;                  // per token
+    const int pos0 = o0 + tile * TG;
+    const int tcount = min(TG, Ts - tile * TG);
+    const int rpad = np * kRowsPerPage;
+    const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
+    const int nst = ceil_div(np, PG);
+    const Job& jb = p.jobs[job];
+    int row = 0;
+    if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
+    for (int k = 0; k < nst; ++k, ++seq) {
+      const unsigned long long t_it = p.trace ? gtimer() : 0;
+      const int stage = seq % NSTAGE;
+      const int pg0 = k * PG;
+      const int npg = min(PG, np - pg0);
+      unsigned char* st = sm.stage[stage];
+      uint32_t bytes = b_bytes * npg;
+      if (k == 0) bytes += tcount * vrow * 4;          // v rows ride on the first stage
+      if (k == nst - 1) bytes += y_bytes * tcount;     // y rows on the last stage
+      if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+      const unsigned long long t_ready = p.trace ? gtimer() : 0;
+      __syncwarp();
+      Meta& m = sm.meta[stage];
+      if (lane == 0) {
+        m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+        m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
+        mbar_arrive_expect_tx(&sm.full[stage], bytes);
+      }
+      if (lane < tcount) m.rows[lane] = row;
+      // B pages of this stage (weights: independent of phase 1 and of the previous kernel)
+      if (lane < npg) {
+        const int pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
+        const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
+        bulk_g2s(st + lane * B_PITCH, src, b_bytes, &sm.full[stage], pol_w);
+      }
+      if (!waited) {  // y may be produced by the previous kernel
+        pdl_wait();
+        pdl_launch_dependents();
+        waited = true;
+      }
+      if (k == nst - 1 && lane < tcount)
+        bulk_g2s(st + K2_Y + lane * NC_BYTES, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes,
+                 &sm.full[stage], pol_w);
+      if (k == 0) {
+        if (!v_ready) {
+          // v of every tile is complete once all CTAs passed the phase-1 barrier
+          if (lane == 0) {
+            while (ld_acquire_gpu(p.ctr + 9) == sm.grid_gen) __nanosleep(32);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+          }
+          __syncwarp();
+          v_ready = true;
+        }
+        if (p.v_in) {
+          if (lane < tcount)
+            bulk_g2s(st + K2_V + lane * vrow * 4, p.v_in + (long long)(pos0 + lane) * p.v_stride, vrow * 4,
+                     &sm.full[stage], pol_w);
+        } else if (lane == 0) {
+          const float* src = p.vws + job * p.vws_job_stride + pl.v_start[s] + (long long)(tile * TG) * rpad;
+          bulk_g2s(st + K2_V, src, tcount * rpad * 4, &sm.full[stage], pol_w);
+        }
+      }
+      if (lane == 0) trace_producer(p, seq, t_it, t_ready, 2, bytes);
+      __syncwarp();
+    }
+  }
+  return seq;
+}
 
-  if (warp == 0) {
-    // ------------------------------------------------------------------ producer
-    const uint64_t pol_w = policy_evict_first();
+// Marker stage between the phases: consumers arrive at the grid barrier on it.
+__device__ __forceinline__ void post_marker(Shared& sm, int seq, int kind) {
+  const int st = seq % NSTAGE;
+  mbar_wait(&sm.empty[st], ((seq / NSTAGE) & 1) ^ 1);
+  sm.meta[st].kind = kind;
+  mbar_arrive(&sm.full[st]);
+}
+
+// Consumers of this CTA finished phase 1: publish (release) and count the CTA in.
+__device__ __forceinline__ void grid_barrier_arrive(const Params& p, const Shared& sm, int ct) {
+  named_bar_sync(1, GROUP_THREADS);  // every consumer thread's v stores precede the arrival
+  if (ct == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + 8, 1) == (int)gridDim.x - 1) {
+      p.ctr[8] = 0;
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ctr + 9), "r"(sm.grid_gen + 1) : "memory");
+    }
+  }
+}
+
+// One launch per lora_apply: phase 1 (shrink units) -> grid barrier -> phase 2 (expand
+// units).  MODE_SHRINK runs phase 1 only (v to v_out), MODE_EXPAND phase 2 only (v_in).
+template <typename T>
+__global__ void __launch_bounds__(NTHREADS, 1) lora_apply_kernel(const __grid_constant__ Params p, int mode) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Shared& sm = *reinterpret_cast<Shared*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) sm.grid_gen = *reinterpret_cast<volatile int*>(p.ctr + 9);
+  int S;
+  if (!prologue(p, sm, S)) {
+    abort_launch(p);
+    return;
+  }
+  const bool fused = mode == MODE_FUSED;
+  // The producer is the highest-numbered warp: the SM's warp schedulers favour higher warp
+  // ids, so the producer is never starved by the FMA-heavy consumer warps on its SMSP.
+  if (warp == GROUP_WARPS) {
     bool waited = false;
     int seq = 0;
-    int next = 0;
-    if (lane == 0) next = atomicAdd(p.ctr, 1);
-    for (;;) {
-      const int unit = __shfl_sync(0xffffffffu, next, 0);
-      if (unit >= total) break;
-      if (lane == 0) next = atomicAdd(p.ctr, 1);
-      const int job = unit / UE;
-      const int rem = unit - job * UE;
-      const int tl = rem / ncc;  // tile index in LPT order
-      const int oi = seg_search(pl.ex_start, NW, tl);
-      const int local = rem - pl.ex_start[oi] * ncc;
-      const int s = pl.order[oi];
-      const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
-      const int slot = pl.seg_sr[s] >> 9;
-      const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
-      const int tile = local / ncc, cc = local - tile * ncc;
-      const int col0 = cc * ncol_unit;
-      const int ncols = min(ncol_unit, p.h_out - col0);
-      const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
-      const uint32_t y_bytes = ncols * ES;                  // per token
-      const int pos0 = o0 + tile * TG;
-      const int tcount = min(TG, Ts - tile * TG);
-      const int rpad = np * kRowsPerPage;
-      const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
-      const int nst = ceil_div(np, PG);
-      const Job& jb = p.jobs[job];
-      int row = 0;
-      if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
-      for (int k = 0; k < nst; ++k, ++seq) {
-        const unsigned long long t_it = p.trace ? gtimer() : 0;
-        const int stage = seq % NSTAGE;
-        const int pg0 = k * PG;
-        const int npg = min(PG, np - pg0);
-        unsigned char* st = sm.stage[stage];
-        uint32_t bytes = b_bytes * npg;
-        if (k == 0) bytes += y_bytes * tcount + tcount * vrow * 4;
-        if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
-        const unsigned long long t_ready = p.trace ? gtimer() : 0;
-        __syncwarp();
-        Meta& m = sm.meta[stage];
-        if (lane == 0) {
-          m.kind = KIND_WORK; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
-          m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
-          mbar_arrive_expect_tx(&sm.full[stage], bytes);
-        }
-        if (lane < tcount) m.rows[lane] = row;
-        // B pages of this stage (weights: no dependency on the shrink kernel)
-        if (lane < npg) {
-          const int pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
-          const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
-          bulk_g2s(st + lane * B_PITCH, src, b_bytes, &sm.full[stage], pol_w);
-        }
-        if (k == 0) {
-          if (lane < tcount)
-            bulk_g2s(st + K2_Y + lane * NC_BYTES, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes,
-                     &sm.full[stage], pol_w);
-          if (!waited) {  // v is produced by the shrink kernel
-            pdl_wait();
-            pdl_launch_dependents();
-            waited = true;
-          }
-          if (p.v_in) {
-            if (lane < tcount)
-              bulk_g2s(st + K2_V + lane * vrow * 4, p.v_in + (long long)(pos0 + lane) * p.v_stride, vrow * 4,
-                       &sm.full[stage], pol_w);
-          } else if (lane == 0) {
-            const float* src = p.vws + job * p.vws_job_stride + pl.v_start[s] + (long long)(tile * TG) * rpad;
-            bulk_g2s(st + K2_V, src, tcount * rpad * 4, &sm.full[stage], pol_w);
-          }
-        }
-        if (lane == 0) trace_producer(p, seq, t_it, t_ready, 2, bytes);
-        __syncwarp();
-      }
+    if (mode != MODE_EXPAND) seq = produce_shrink<T>(p, sm, seq, waited);
+    if (fused) {
+      if (lane == 0) post_marker(sm, seq, KIND_PHASE);
+      ++seq;
     }
+    if (mode != MODE_SHRINK) seq = produce_expand<T>(p, sm, seq, waited, fused);
     if (!waited) pdl_wait();
-    if (lane == 0) post_end(sm, seq);
+    if (lane == 0) post_marker(sm, seq, KIND_END);
   } else {
-    // ------------------------------------------------------------------ consumers
-    const int ct = tid - 32;
+    const int ct = tid;  // consumer warps 0 .. GROUP_WARPS-1
+    const int gw = ct >> 5;
+    float* red = reinterpret_cast<float*>(sm.scratch);
     int seq = 0;
     for (;;) {
       const int stage = seq % NSTAGE;
       mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
       const Meta m0 = sm.meta[stage];
       if (m0.kind == KIND_END) break;
-      switch (m0.T) {
-        case 1: expand_unit<T, 1>(p, sm, seq, m0, ct); break;
-        case 2: expand_unit<T, 2>(p, sm, seq, m0, ct); break;
-        case 3: expand_unit<T, 3>(p, sm, seq, m0, ct); break;
-        default: expand_unit<T, 4>(p, sm, seq, m0, ct); break;
+      if (m0.kind == KIND_PHASE) {
+        grid_barrier_arrive(p, sm, ct);
+        mbar_arrive(&sm.empty[stage]);
+        ++seq;
+        continue;
+      }
+      if (m0.kind == KIND_SHRINK) {
+        switch (m0.T) {
+          case 1: shrink_unit<T, 1>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
+          case 2: shrink_unit<T, 2>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
+          case 3: shrink_unit<T, 3>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
+          default: shrink_unit<T, 4>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
+        }
+      } else {
+        switch (m0.T) {
+          case 1: expand_unit<T, 1>(p, sm, seq, m0, ct); break;
+          case 2: expand_unit<T, 2>(p, sm, seq, m0, ct); break;
+          case 3: expand_unit<T, 3>(p, sm, seq, m0, ct); break;
+          default: expand_unit<T, 4>(p, sm, seq, m0, ct); break;
+        }
       }
     }
   }
-  reset_counter_if_last(p);
+  // the last CTA re-arms both unit counters for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[4] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // One CTA builds the step's plan and writes it to global memory (consumed by every
@@ -780,8 +869,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) build_plan_kernel(const __grid_co
   for (int i = threadIdx.x; i < (int)(sizeof(Plan) / 16); i += NTHREADS) dst[i] = src[i];
 }
 
-template <typename KernelT>
-int launch_pdl(KernelT kern, int smem, const cham_pool* pool, const Params& prm, cudaStream_t stream) {
+template <typename T>
+int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
+  static bool attr_set[2] = {false, false};
+  auto kern = lora_apply_kernel<T>;
+  const int smem = sizeof(Shared);
+  if (!attr_set[Elem<T>::kDtype]) {
+    CHAM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set[Elem<T>::kDtype] = true;
+  }
+  // ping-pong v workspace: apply n uses buffer n % 2 (see the ordering argument above)
+  prm.vws_job_stride = (long long)pool->max_tokens * kMaxRank;
+  prm.vws = pool->d_vws + (pool->apply_count & 1) * (size_t)kMaxJobs * prm.vws_job_stride;
+  // counters ping-pong like the v buffer: apply n+1 may start (PDL) while apply n's last
+  // CTA is still re-arming its own counter set
+  prm.ctr = pool->d_ctr + 16 + (pool->apply_count & 1) * 16;
+  prm.err = pool->d_ctr + 2;
+  ++pool->apply_count;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pool->sm_count);
   cfg.blockDim = dim3(NTHREADS);
@@ -792,36 +896,8 @@ int launch_pdl(KernelT kern, int smem, const cham_pool* pool, const Params& prm,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CHAM_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  CHAM_CUDA(cudaLaunchKernelEx(&cfg, kern, prm, mode));
   return CHAM_OK;
-}
-
-template <typename T>
-int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
-  static bool attr_set[2] = {false, false};
-  auto k1 = lora_shrink_kernel<T>;
-  auto k2 = lora_expand_kernel<T>;
-  const int s1 = sizeof(K1Shared), s2 = sizeof(K2Shared);
-  if (!attr_set[Elem<T>::kDtype]) {
-    CHAM_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
-    CHAM_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
-    attr_set[Elem<T>::kDtype] = true;
-  }
-  // ping-pong v workspace: apply n uses buffer n % 2 (see the ordering argument above)
-  Params p1 = prm;
-  p1.vws_job_stride = (long long)pool->max_tokens * kMaxRank;
-  p1.vws = pool->d_vws + (pool->apply_count & 1) * (size_t)kMaxJobs * p1.vws_job_stride;
-  p1.ctr = pool->d_ctr;
-  p1.err = pool->d_ctr + 2;
-  Params p2 = p1;
-  p2.ctr = pool->d_ctr + 4;
-  if (p2.trace) p2.trace += (size_t)pool->sm_count * p2.trace_cap * 8;  // K2 timeline in the second half
-  ++pool->apply_count;
-  if (mode != MODE_EXPAND) {
-    int rc = launch_pdl(k1, s1, pool, p1, stream);
-    if (rc || mode == MODE_SHRINK) return rc;
-  }
-  return launch_pdl(k2, s2, pool, p2, stream);
 }
 
 }  // namespace decode

@@ -176,13 +176,13 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   }
   e = cudaMalloc(&pool->d_slot_pages, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   if (e == cudaSuccess) e = cudaMalloc(&pool->d_slot_rank, sizeof(int) * (size_t)n_slots);
-  if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 48);
   if (e == cudaSuccess)
     e = cudaMalloc(&pool->d_vws, 2 * sizeof(float) * (size_t)kMaxJobs * max_tokens * kMaxRank);
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);
-  cudaMemset(pool->d_ctr, 0, sizeof(int) * 8);
+  cudaMemset(pool->d_ctr, 0, sizeof(int) * 48);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cleanup(CHAM_ERR_CUDA, std::string("cham_pool_create: ") + cudaGetErrorString(e));
   cudaSetDevice(prev);

@@ -24,7 +24,7 @@ struct cham_pool {
   std::vector<int> slot_rank;          // host mirror
   std::vector<int> slot_pages;         // host mirror [n_slots][kMaxPagesPerSlot]
   // decode / shrink / expand workspace (one launch at a time per pool)
-  int* d_ctr = nullptr;                // [0,1] shrink: next item, finished CTAs; [2] error; [4,5] expand
+  int* d_ctr = nullptr;                // [2] error; [16..31] / [32..47]: per-parity launch counters
   float* d_vws = nullptr;              // 2 x [kMaxJobs][max_tokens][vws_kc][kMaxRank] (ping-pong)
   int vws_kc = 1;
   unsigned long long apply_count = 0;  // selects the v ping-pong buffer

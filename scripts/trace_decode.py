@@ -77,6 +77,10 @@ def analyze(tr, name):
     post = (issue - rd)[valid]
     print(f"  producer: iteration-start -> stage free us p50 {np.median(pre)/1e3:.2f} p90 {np.percentile(pre,90)/1e3:.2f}; "
           f"stage free -> copies issued us p50 {np.median(post)/1e3:.2f} p90 {np.percentile(post,90)/1e3:.2f}")
+    m6 = valid & (tr[:, :, 6] > 0)
+    if m6.any():
+        print(f"  producer unit prologue: dispatch us p50 {np.median(tr[:, :, 6][m6])/1e3:.2f} p90 {np.percentile(tr[:, :, 6][m6], 90)/1e3:.2f}; "
+              f"decode us p50 {np.median(tr[:, :, 7][m6])/1e3:.2f} p90 {np.percentile(tr[:, :, 7][m6], 90)/1e3:.2f}")
     prev_issue_to_it = (it[:, 1:] - issue[:, :-1])[valid[:, 1:] & valid[:, :-1]]
     print(f"  producer: previous issue -> next iteration start us p50 {np.median(prev_issue_to_it)/1e3:.2f}")
     last_end = np.array([end[c, :per_cta[c]].max() if per_cta[c] else 0 for c in range(n_cta)])
@@ -110,14 +114,17 @@ def main():
         else:
             lora_apply_table(xs[1], ys[3], ex.table, pool=pool, layer=7, proj=3)
         torch.cuda.synchronize()
-        tr = buf.cpu().numpy()
+        tr = buf.cpu().numpy()[0]
         np.save(out / f"trace_{name}.npy", tr)
-        t0 = tr[:, :, :, 0][tr[:, :, :, 0] > 0].min()
-        for k, kn in ((0, "shrink kernel"), (1, "expand kernel")):
-            sub = tr[k].copy()
-            valid = sub[:, :, 0] > 0
-            print(f"   [{kn}] starts {(sub[:, :, 0][valid].min() - t0) / 1e3:.1f} us after the first issue")
-            analyze(sub, f"{name} {kn}")
+        analyze(tr, f"{name} fused kernel")
+        valid = tr[:, :, 0] > 0
+        t0 = tr[:, :, 0][valid].min()
+        kind = tr[:, :, 1] >> 32
+        for k, kn in ((1, "shrink"), (2, "expand")):
+            m = valid & (kind == k)
+            if m.any():
+                print(f"   {kn} phase: first issue {(tr[:, :, 0][m].min() - t0) / 1e3:.1f} us, last consumer end "
+                      f"{(tr[:, :, 3][m].max() - t0) / 1e3:.1f} us")
     _lib.call("cham_debug_set_trace", pool.handle, None, 0)
 
 
