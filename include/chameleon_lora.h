@@ -148,12 +148,13 @@ CHAM_API int cham_lora_apply(cham_pool* pool, int layer, int proj, const void* x
                     int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
                     const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream);
 
-/* Launch plan (segment prefix sums, largest-rank-first order, page ids, perm) for one
- * segment table against the pool's current slot table, built on the device by one CTA.
- * Valid while the slots of the batch stay bound (their adapters are pinned for the step),
- * so one plan serves every (layer, projection) apply of a step.  `plan` is device memory of
- * cham_plan_bytes() bytes, 16-byte aligned. */
-CHAM_API size_t cham_plan_bytes(void);
+/* Launch plan for one segment table against the pool's current slot table, built on the
+ * device by one CTA: segment prefix sums, largest-rank-first order, page ids, perm, and a
+ * 32-byte work descriptor per shrink unit / expand tile.  Valid while the slots of the batch
+ * stay bound (their adapters are pinned for the step), so one plan serves every
+ * (layer, projection) apply of a step.  `plan` is device memory of cham_plan_bytes(pool)
+ * bytes, 16-byte aligned. */
+CHAM_API size_t cham_plan_bytes(const cham_pool* pool);
 CHAM_API int cham_build_plan(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
                              const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan,
                              void* stream);

@@ -55,7 +55,7 @@ SIGNATURES = {
     "cham_pack_adapter_host": (c_int, [_P, c_int, _P, _P, _P]),
     "cham_pack_adapter_device": (c_int, [_P, c_int, _P, _P, _P, _P]),
     "cham_build_segments": (c_int, [_P, _P, _P, c_int, _P, _P, _P, _P, _P, _P]),
-    "cham_plan_bytes": (c_size_t, []),
+    "cham_plan_bytes": (c_size_t, [_P]),
     "cham_build_plan": (c_int, [_P, _P, _P, _P, _P, c_int, _P, _P, _P]),
     "cham_lora_apply": (c_int, [_P, c_int, c_int, _P, _P, c_int, _P, _P, _P, _P, c_int, _P, _P, _P]),
     "cham_lora_apply_multi": (c_int, [_P, c_int, c_int, _IP, POINTER(_P), POINTER(_P), c_int, _P, _P, _P, _P,

@@ -6,7 +6,7 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
                  void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
                  const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream, int mode,
                  float* v_out, const float* v_in, int v_stride);
-size_t plan_bytes();
+size_t plan_bytes(const cham_pool* pool);
 int build_plan_entry(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
                      const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan, void* stream);
 }
@@ -53,7 +53,7 @@ int cham_lora_expand(cham_pool* pool, int layer, int proj, const float* v, int v
                       n_seg_dev, plan, stream, /*MODE_EXPAND*/ 2, nullptr, v, v_stride);
 }
 
-size_t cham_plan_bytes(void) { return plan_bytes(); }
+size_t cham_plan_bytes(const cham_pool* pool) { return pool ? plan_bytes(pool) : 0; }
 
 int cham_build_plan(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
                     const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan, void* stream) {
@@ -61,5 +61,7 @@ int cham_build_plan(cham_pool* pool, const int* perm, const int* seg_off, const 
 }
 
 int cham_prefill_min_tokens_internal() { return 1 << 30; }
+
+size_t cham_plan_bytes_internal(const cham_pool* pool) { return plan_bytes(pool); }
 
 }  // extern "C"

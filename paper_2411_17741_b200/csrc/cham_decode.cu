@@ -90,7 +90,8 @@ struct Params {
   int v_stride;
   unsigned long long* trace;  // debug: [cta][seq][8] globaltimer stamps (null = off)
   int trace_cap;
-  const void* plan;           // prebuilt Plan (cham_build_plan) or null: build in the kernel
+  const void* plan;           // Plan header + unit descriptors (cham_build_plan)
+  long long desc_cap;
 };
 
 // Per-stage record written by the producer, read by the consumers after the full barrier.
@@ -121,9 +122,26 @@ struct alignas(16) Plan {
   int scan[NTHREADS / 32][4];
   int totals[6];  // K1 units/job, K2 tiles/job, tokens, pages, v floats/job, segments with work
   int n_seg;
-  int pad;
+  int order_pos[PLAN_SEGS];  // segment -> position in the LPT order
+  long long desc_cap;        // descriptor capacity (entries) after the header
 };
 static_assert(sizeof(Plan) % 16 == 0, "the plan is moved with one bulk copy");
+
+// 32-byte work descriptors written by the plan kernel right after the Plan header:
+// first one per shrink unit (job-independent, segment order), then one per expand tile
+// (LPT order).  The producer fetches the descriptor of unit k+1 while it streams unit k.
+struct alignas(16) UnitDesc {
+  int seg;
+  int pos0;
+  int meta;     // tcount | np << 8 | g << 16   (g: shrink page index)
+  int aux;      // shrink: pool page id of page g; expand: offset of the tile's v rows
+  int rows[TG]; // token rows of the tile (perm)
+};
+static_assert(sizeof(UnitDesc) == 32, "descriptor layout");
+__host__ __device__ inline long long plan_desc_capacity(int max_tokens) {
+  // shrink units <= T * kMaxPagesPerSlot, expand tiles <= T
+  return (long long)max_tokens * (kMaxPagesPerSlot + 1);
+}
 
 constexpr int STAGE_BYTES = K1_STAGE > K2_STAGE ? K1_STAGE : K2_STAGE;
 constexpr int SCRATCH_BYTES = TG * kMaxRank * 4;  // K2 v rows; K1 uses the first 1 KiB
@@ -201,7 +219,7 @@ __device__ __forceinline__ int n_colchunks(const Params& p) {
 
 // Builds the launch plan in shared memory (all NTHREADS threads).  It depends only on the
 // segment table and the slot table, so one plan serves every (layer, projection) of a step.
-__device__ bool build_plan(const Params& p, Plan& pl, int S) {
+__device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < kMaxPagesPerSlot + 2) pl.bucket[tid] = 0;
   const int per = ceil_div(S, NTHREADS);
@@ -273,7 +291,11 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S) {
   for (int s = s0; s < s1; ++s) {
     const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
     const int T_s = pl.seg_off[s + 1] - pl.seg_off[s];
-    if (np > 0 && T_s > 0) pl.order[atomicAdd(&pl.bucket[np], 1)] = s;
+    if (np > 0 && T_s > 0) {
+      const int oi = atomicAdd(&pl.bucket[np], 1);
+      pl.order[oi] = s;
+      pl.order_pos[s] = oi;
+    }
   }
   if (pl.totals[3] <= PLAN_PAGES) {
     for (int s = s0; s < s1; ++s) {
@@ -314,6 +336,36 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S) {
     }
   }
   __syncthreads();
+  if (desc) {
+    // descriptors: shrink units [0, totals[0]) then expand tiles [totals[0], + totals[1])
+    if ((long long)pl.totals[0] + pl.totals[1] > p.desc_cap) return false;
+    UnitDesc* dex = desc + pl.totals[0];
+    for (int s = s0; s < s1; ++s) {
+      const int o0 = pl.seg_off[s], T_s = pl.seg_off[s + 1] - o0;
+      const int slot = pl.seg_sr[s] >> 9;
+      const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
+      if (np == 0 || T_s == 0) continue;
+      const int nt = ceil_div(T_s, TG);
+      for (int t = 0; t < nt; ++t) {
+        UnitDesc d;
+        d.seg = s;
+        d.pos0 = o0 + t * TG;
+        const int tc = min(TG, T_s - t * TG);
+        for (int i = 0; i < TG; ++i) {
+          const int pos = d.pos0 + min(i, tc - 1);
+          d.rows[i] = p.perm ? __ldg(p.perm + pos) : pos;
+        }
+        for (int g = 0; g < np; ++g) {
+          d.meta = tc | (np << 8) | (g << 16);
+          d.aux = __ldg(p.slot_pages + slot * kMaxPagesPerSlot + g);
+          desc[pl.sh_start[s] + t * np + g] = d;
+        }
+        d.meta = tc | (np << 8);
+        d.aux = pl.v_start[s] + t * TG * np * kRowsPerPage;
+        dex[pl.ex_start[pl.order_pos[s]] + t] = d;
+      }
+    }
+  }
   return true;
 }
 
@@ -326,10 +378,9 @@ __device__ __forceinline__ int row_of(const Params& p, const Plan& pl, bool perm
 
 
 
-// Barriers + plan.  A prebuilt plan is pulled into shared memory with one bulk copy (the
-// plan is written by an earlier kernel of the step, so it may be read before the PDL wait).
-template <class SH>
-__device__ __forceinline__ bool prologue(const Params& p, SH& sm, int& S_out) {
+// Barriers + plan header (one bulk copy; the plan was written by an earlier kernel of the
+// step, so it may be read before the PDL wait).
+__device__ __forceinline__ bool prologue(const Params& p, Shared& sm) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(&sm.full[i], 1);
@@ -337,21 +388,12 @@ __device__ __forceinline__ bool prologue(const Params& p, SH& sm, int& S_out) {
     }
     mbar_init(&sm.plan_bar, 1);
     fence_mbar_init();
-    if (p.plan) {
-      mbar_arrive_expect_tx(&sm.plan_bar, sizeof(Plan));
-      bulk_g2s(&sm.plan, p.plan, sizeof(Plan), &sm.plan_bar, policy_evict_last());
-    }
+    mbar_arrive_expect_tx(&sm.plan_bar, sizeof(Plan));
+    bulk_g2s(&sm.plan, p.plan, sizeof(Plan), &sm.plan_bar, policy_evict_last());
   }
   __syncthreads();
-  if (p.plan) {
-    mbar_wait(&sm.plan_bar, 0);
-    S_out = sm.plan.totals[5] >= 0 ? 1 : 0;  // unused with a prebuilt plan
-    return sm.plan.totals[2] <= p.max_tokens;
-  }
-  const int S = p.n_seg >= 0 ? p.n_seg : *p.n_seg_dev;
-  S_out = S;
-  if (S > PLAN_SEGS || S < 0) return false;
-  return build_plan(p, sm.plan, S);
+  mbar_wait(&sm.plan_bar, 0);
+  return sm.plan.totals[2] <= p.max_tokens;
 }
 
 __device__ __forceinline__ void abort_launch(const Params& p) {
@@ -478,22 +520,34 @@ __device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& 
       named_bar_sync(1, GROUP_THREADS);
     }
     if (active) {
-      // two pages per stage: thread h takes page pg0+h; a single page is split in row halves
-      const int nrow = m.npg == 2 ? kRowsPerPage : kRowsPerPage / 2;
-      const int r0 = m.npg == 2 ? 0 : h * (kRowsPerPage / 2);
+      // two pages per stage: thread h takes page pg0+h (two row halves); a single page is
+      // split in row halves between h = 0 and h = 1.  Halves of 4 rows are fully unrolled.
       const int pgl = m.npg == 2 ? h : 0;
+      const int hbeg = m.npg == 2 ? 0 : h;
+      const int hend = m.npg == 2 ? 2 : h + 1;
       const unsigned char* Bg = st + pgl * B_PITCH;
       const int vbase = (m.pg0 + pgl) * kRowsPerPage;
-      for (int j = r0; j < r0 + nrow; ++j) {
-        float2 bf[NP2];
-        Elem<T>::unpack2(lds128(Bg + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf);
+      for (int hh = hbeg; hh < hend; ++hh) {
+        float vv[NT][4];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          const float vv = vs[t * kMaxRank + vbase + j];
-          const float2 v2 = make_float2(vv, vv);
-#pragma unroll
-          for (int e = 0; e < NP2; ++e) acc[t][e] = __ffma2_rn(v2, bf[e], acc[t][e]);
+          const float4 v4 = *reinterpret_cast<const float4*>(vs + t * kMaxRank + vbase + hh * 4);
+          vv[t][0] = v4.x; vv[t][1] = v4.y; vv[t][2] = v4.z; vv[t][3] = v4.w;
         }
+        float2 bf[4][NP2];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = hh * 4 + jj;
+          Elem<T>::unpack2(lds128(Bg + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf[jj]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const float2 v2 = make_float2(vv[t][jj], vv[t][jj]);
+#pragma unroll
+            for (int e = 0; e < NP2; ++e) acc[t][e] = __ffma2_rn(v2, bf[jj][e], acc[t][e]);
+          }
       }
     }
     if (k == m0.nst - 1) {
@@ -578,47 +632,39 @@ struct UnitQueue {
   }
 };
 
+__device__ __forceinline__ void ldg_desc(const UnitDesc* d, int4& a, int4& b) {
+  const int4* q = reinterpret_cast<const int4*>(d);
+  a = __ldg(q);
+  b = __ldg(q + 1);
+}
+
 template <typename T>
 __device__ __forceinline__ int produce_shrink(const Params& p, Shared& sm, int seq, bool& waited) {
   constexpr int ES = Elem<T>::kBytes;
-  const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
-  const int S = pl.n_seg;
-  const int US = pl.totals[0];
-  const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
-  const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
+  const int US = sm.plan.totals[0];
   const int total = p.n_jobs * US;
   const int nkc = n_kchunks<T>(p);
   const int natoms = p.h_in * ES / kRowBytes;
+  const UnitDesc* desc = reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan));
   const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
   const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page of the tile
   UnitQueue uq;
-  uq.init(p.ctr, total, 3, lane, &sm.unit_mailbox);  // uniform units: prefetch two ahead
-  for (;;) {
-    const unsigned long long t_u0 = p.trace ? gtimer() : 0;
-    const int unit = uq.next(lane);
-    if (unit < 0) break;
-    const unsigned long long t_u1 = p.trace ? gtimer() : 0;
+  uq.init(p.ctr, total, 3, lane, &sm.unit_mailbox);
+  int unit = uq.next(lane);
+  int4 da = make_int4(0, 0, 0, 0), db = da;
+  if (unit >= 0) ldg_desc(desc + unit % US, da, db);
+  while (unit >= 0) {
+    // prefetch the next unit's descriptor while this one streams
+    const int nunit = uq.next(lane);
+    int4 na = da, nb = db;
+    if (nunit >= 0) ldg_desc(desc + nunit % US, na, nb);
     const int job = unit / US;
-    const int rem = unit - job * US;
-    const int s = seg_search(pl.sh_start, S, rem);
-    const int local = rem - pl.sh_start[s];
-    const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
-    const int slot = pl.seg_sr[s] >> 9;
-    const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
-    const int tile = local / np, g = local - tile * np;
-    const int pos0 = o0 + tile * TG;
-    const int tcount = min(TG, Ts - tile * TG);
+    const int s = da.x, pos0 = da.y;
+    const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff, g = da.z >> 16;
+    const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
     const Job& jb = p.jobs[job];
-    int row = 0;
-    if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
-    const int pg = page_of(p, pl, pages_smem, s, slot, g);
-    const char* a_src = p.base + (long long)pg * p.page_bytes + jb.a_off;
-    const unsigned long long t_u2 = p.trace ? gtimer() : 0;
-    if (p.trace && lane == 0 && seq < p.trace_cap) {
-      p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 6] = (t_u1 - t_u0);
-      p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 7] = (t_u2 - t_u1);
-    }
+    const char* a_src = p.base + (long long)da.w * p.page_bytes + jb.a_off;
     for (int kc = 0; kc < nkc; ++kc, ++seq) {
       const unsigned long long t_it = p.trace ? gtimer() : 0;
       const int stage = seq % NSTAGE;
@@ -648,6 +694,9 @@ __device__ __forceinline__ int produce_shrink(const Params& p, Shared& sm, int s
       if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
       __syncwarp();
     }
+    unit = nunit;
+    da = na;
+    db = nb;
   }
   return seq;
 }
@@ -660,41 +709,42 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
   const int ncc = n_colchunks<T>(p);
-  const int UE = pl.totals[1] * ncc;
-  const int NW = pl.totals[5];
+  const int NTL = pl.totals[1];  // tiles per job
+  const int UE = NTL * ncc;
   const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
-  const bool perm_smem = pl.totals[2] <= PLAN_TOKENS;
   const int total = p.n_jobs * UE;
   const int ncol_unit = NC_BYTES / ES;
+  const UnitDesc* desc =
+      reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan)) + pl.totals[0];
   const uint64_t pol_w = policy_evict_first();
   bool v_ready = !fused;
   UnitQueue uq;
-  uq.init(p.ctr + 4, total, 2, lane, &sm.unit_mailbox);  // variable units: one ahead keeps the LPT balance
-  for (;;) {
-    const int unit = uq.next(lane);
-    if (unit < 0) break;
-    const int job = unit / UE;
-    const int rem = unit - job * UE;
-    const int tl = rem / ncc;  // tile index in LPT order
-    const int oi = seg_search(pl.ex_start, NW, tl);
-    const int local = rem - pl.ex_start[oi] * ncc;
-    const int s = pl.order[oi];
-    const int o0 = pl.seg_off[s], Ts = pl.seg_off[s + 1] - o0;
+  uq.init(p.ctr + 4, total, 2, lane, &sm.unit_mailbox);
+  int unit = uq.next(lane);
+  int4 da = make_int4(0, 0, 0, 0), db = da;
+  // unit = (tile_lpt * n_jobs + job) * ncc + cc: largest-rank tiles of every job first
+  const int per_tile = p.n_jobs * ncc;
+  if (unit >= 0) ldg_desc(desc + unit / per_tile, da, db);
+  while (unit >= 0) {
+    const int nunit = uq.next(lane);
+    int4 na = da, nb = db;
+    if (nunit >= 0) ldg_desc(desc + nunit / per_tile, na, nb);
+    const int jc = unit % per_tile;
+    const int job = jc / ncc;
+    const int cc = jc - job * ncc;
+    const int s = da.x, pos0 = da.y;
+    const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff;
+    const int vbase = da.w;
+    const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
     const int slot = pl.seg_sr[s] >> 9;
-    const int np = ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
-    const int tile = local / ncc, cc = local - tile * ncc;
     const int col0 = cc * ncol_unit;
     const int ncols = min(ncol_unit, p.h_out - col0);
     const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
     const uint32_t y_bytes = ncols * ES;                  // per token
-    const int pos0 = o0 + tile * TG;
-    const int tcount = min(TG, Ts - tile * TG);
     const int rpad = np * kRowsPerPage;
     const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
     const int nst = ceil_div(np, PG);
     const Job& jb = p.jobs[job];
-    int row = 0;
-    if (lane < tcount) row = row_of(p, pl, perm_smem, pos0 + lane);
     for (int k = 0; k < nst; ++k, ++seq) {
       const unsigned long long t_it = p.trace ? gtimer() : 0;
       const int stage = seq % NSTAGE;
@@ -704,6 +754,8 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
       uint32_t bytes = b_bytes * npg;
       if (k == 0) bytes += tcount * vrow * 4;          // v rows ride on the first stage
       if (k == nst - 1) bytes += y_bytes * tcount;     // y rows on the last stage
+      int pgid = 0;
+      if (lane < npg) pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
       if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
       const unsigned long long t_ready = p.trace ? gtimer() : 0;
       __syncwarp();
@@ -716,7 +768,6 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
       if (lane < tcount) m.rows[lane] = row;
       // B pages of this stage (weights: independent of phase 1 and of the previous kernel)
       if (lane < npg) {
-        const int pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
         const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
         bulk_g2s(st + lane * B_PITCH, src, b_bytes, &sm.full[stage], pol_w);
       }
@@ -743,13 +794,15 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
             bulk_g2s(st + K2_V + lane * vrow * 4, p.v_in + (long long)(pos0 + lane) * p.v_stride, vrow * 4,
                      &sm.full[stage], pol_w);
         } else if (lane == 0) {
-          const float* src = p.vws + job * p.vws_job_stride + pl.v_start[s] + (long long)(tile * TG) * rpad;
-          bulk_g2s(st + K2_V, src, tcount * rpad * 4, &sm.full[stage], pol_w);
+          bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase, tcount * rpad * 4, &sm.full[stage], pol_w);
         }
       }
       if (lane == 0) trace_producer(p, seq, t_it, t_ready, 2, bytes);
       __syncwarp();
     }
+    unit = nunit;
+    da = na;
+    db = nb;
   }
   return seq;
 }
@@ -783,8 +836,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_apply_kernel(const __grid_co
   Shared& sm = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) sm.grid_gen = *reinterpret_cast<volatile int*>(p.ctr + 9);
-  int S;
-  if (!prologue(p, sm, S)) {
+  if (!prologue(p, sm)) {
     abort_launch(p);
     return;
   }
@@ -855,7 +907,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) build_plan_kernel(const __grid_co
   Plan& pl = *reinterpret_cast<Plan*>(smem_raw);
   const int S = p.n_seg >= 0 ? p.n_seg : *p.n_seg_dev;
   bool ok = S >= 0 && S <= PLAN_SEGS;
-  if (ok) ok = build_plan(p, pl, S);
+  if (ok) ok = build_plan(p, pl, S, reinterpret_cast<UnitDesc*>(out + 1));
+  if (threadIdx.x == 0) pl.desc_cap = p.desc_cap;
   __syncthreads();
   if (!ok) {
     if (threadIdx.x == 0) {
@@ -901,6 +954,33 @@ int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
 }
 
 }  // namespace decode
+
+size_t plan_bytes(const cham_pool* pool) {
+  return sizeof(decode::Plan) + sizeof(decode::UnitDesc) * (size_t)decode::plan_desc_capacity(pool->max_tokens);
+}
+
+int build_plan_entry(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
+                     const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan, void* stream) {
+  using namespace decode;
+  if (!pool || !plan || !seg_off || !seg_slot || !seg_rank) return fail(CHAM_ERR_INVALID, "cham_build_plan: null argument");
+  if (n_seg < 0 && !n_seg_dev) return fail(CHAM_ERR_INVALID, "cham_build_plan: n_seg < 0 needs n_seg_dev");
+  if (n_seg > PLAN_SEGS) return fail(CHAM_ERR_LIMIT, "cham_build_plan: too many segments");
+  if (reinterpret_cast<uintptr_t>(plan) & 15) return fail(CHAM_ERR_INVALID, "cham_build_plan: plan must be 16-byte aligned");
+  Params prm{};
+  prm.slot_pages = pool->d_slot_pages;
+  prm.perm = perm;
+  prm.seg_off = seg_off;
+  prm.seg_slot = seg_slot;
+  prm.seg_rank = seg_rank;
+  prm.n_seg = n_seg;
+  prm.n_seg_dev = n_seg_dev;
+  prm.max_tokens = pool->max_tokens;
+  prm.err = pool->d_ctr + 2;
+  prm.desc_cap = plan_desc_capacity(pool->max_tokens);
+  build_plan_kernel<<<1, NTHREADS, sizeof(Plan), (cudaStream_t)stream>>>(prm, static_cast<Plan*>(plan));
+  CHAM_CUDA(cudaGetLastError());
+  return CHAM_OK;
+}
 
 // Shared validation + parameter setup for the four entry points.
 int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
@@ -956,35 +1036,16 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   prm.v_stride = v_stride;
   prm.trace = pool->d_trace;
   prm.trace_cap = pool->trace_cap;
+  prm.desc_cap = plan_desc_capacity(pool->max_tokens);
+  if (!plan) {
+    // no step-level plan: build one for this call into the pool's scratch plan
+    int rc = build_plan_entry(pool, perm, seg_off, seg_slot, seg_rank, n_seg, n_seg_dev, pool->d_plan, stream);
+    if (rc) return rc;
+    plan = pool->d_plan;
+  }
   prm.plan = plan;
   if (pool->dtype == CHAM_BF16) return launch<__nv_bfloat16>(pool, prm, mode, (cudaStream_t)stream);
   return launch<float>(pool, prm, mode, (cudaStream_t)stream);
 }
 
-}  // namespace cham
-
-namespace cham {
-size_t plan_bytes() { return sizeof(decode::Plan); }
-
-int build_plan_entry(cham_pool* pool, const int* perm, const int* seg_off, const int* seg_slot,
-                     const int* seg_rank, int n_seg, const int* n_seg_dev, void* plan, void* stream) {
-  using namespace decode;
-  if (!pool || !plan || !seg_off || !seg_slot || !seg_rank) return fail(CHAM_ERR_INVALID, "cham_build_plan: null argument");
-  if (n_seg < 0 && !n_seg_dev) return fail(CHAM_ERR_INVALID, "cham_build_plan: n_seg < 0 needs n_seg_dev");
-  if (n_seg > PLAN_SEGS) return fail(CHAM_ERR_LIMIT, "cham_build_plan: too many segments");
-  if (reinterpret_cast<uintptr_t>(plan) & 15) return fail(CHAM_ERR_INVALID, "cham_build_plan: plan must be 16-byte aligned");
-  Params prm{};
-  prm.slot_pages = pool->d_slot_pages;
-  prm.perm = perm;
-  prm.seg_off = seg_off;
-  prm.seg_slot = seg_slot;
-  prm.seg_rank = seg_rank;
-  prm.n_seg = n_seg;
-  prm.n_seg_dev = n_seg_dev;
-  prm.max_tokens = pool->max_tokens;
-  prm.err = pool->d_ctr + 2;
-  build_plan_kernel<<<1, NTHREADS, sizeof(Plan), (cudaStream_t)stream>>>(prm, static_cast<Plan*>(plan));
-  CHAM_CUDA(cudaGetLastError());
-  return CHAM_OK;
-}
 }  // namespace cham

@@ -160,6 +160,7 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_slot_rank);
     cudaFree(pool->d_ctr);
     cudaFree(pool->d_vws);
+    cudaFree(pool->d_plan);
     delete pool;
     cudaSetDevice(prev);
     return fail(code, msg);
@@ -179,6 +180,10 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 48);
   if (e == cudaSuccess)
     e = cudaMalloc(&pool->d_vws, 2 * sizeof(float) * (size_t)kMaxJobs * max_tokens * kMaxRank);
+  if (e == cudaSuccess) {
+    extern size_t cham_plan_bytes_internal(const cham_pool*);
+    e = cudaMalloc(&pool->d_plan, cham_plan_bytes_internal(pool));
+  }
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);
@@ -198,6 +203,7 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_slot_rank);
   cudaFree(pool->d_ctr);
   cudaFree(pool->d_vws);
+  cudaFree(pool->d_plan);
   delete pool;
   return CHAM_OK;
 }

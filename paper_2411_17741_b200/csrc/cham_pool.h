@@ -27,7 +27,8 @@ struct cham_pool {
   int* d_ctr = nullptr;                // [2] error; [16..31] / [32..47]: per-parity launch counters
   float* d_vws = nullptr;              // 2 x [kMaxJobs][max_tokens][vws_kc][kMaxRank] (ping-pong)
   int vws_kc = 1;
-  unsigned long long apply_count = 0;  // selects the v ping-pong buffer
+  unsigned long long apply_count = 0;  // selects the v / counter ping-pong sets
+  void* d_plan = nullptr;              // scratch plan for calls without a step-level plan
   unsigned long long* d_trace = nullptr;  // debug timeline buffer (caller-owned)
   int trace_cap = 0;
 };

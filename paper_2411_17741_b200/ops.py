@@ -83,15 +83,15 @@ def build_segments(req_slot, req_rank, req_ntok, *, device=None, stream=None,
     return out
 
 
-def plan_bytes() -> int:
-    return int(_lib.lib().cham_plan_bytes())
+def plan_bytes(pool: AdapterPool) -> int:
+    return int(_lib.lib().cham_plan_bytes(pool.handle))
 
 
 def build_plan(table: SegmentTable, *, pool: AdapterPool, stream=None) -> torch.Tensor:
     """Device launch plan for `table` against the pool's slot table (one CTA).  Every
     lora_apply of the step reuses it, so the kernels skip their own plan construction."""
     if table.plan is None:
-        table.plan = torch.empty(plan_bytes(), dtype=torch.uint8, device=pool.device)
+        table.plan = torch.empty(plan_bytes(pool), dtype=torch.uint8, device=pool.device)
     call("cham_build_plan", pool.handle, table.perm.data_ptr(), table.seg_off.data_ptr(), table.seg_slot.data_ptr(),
          table.seg_rank.data_ptr(), -1 if table.n_seg_host is None else table.n_seg_host, table.n_seg.data_ptr(),
          table.plan.data_ptr(), _stream_ptr(stream))
