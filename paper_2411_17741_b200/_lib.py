@@ -10,7 +10,10 @@ import ctypes
 from ctypes import POINTER, c_int, c_size_t, c_void_p, c_char_p
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libchameleon_lora.so")
+import os
+
+# CHAM_LIB overrides the in-tree library (used for A/B builds in experiments only)
+LIB_PATH = Path(os.environ.get("CHAM_LIB") or Path(__file__).resolve().with_name("libchameleon_lora.so"))
 
 CHAM_F32 = 0
 CHAM_BF16 = 1

@@ -27,17 +27,18 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA extension cannot be built")
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, out: Path = None, defines=()) -> Path:
     srcs = [HERE / s for s in SOURCES if (HERE / s).exists()]
     deps = srcs + list(HERE.glob("*.cuh")) + list(HERE.glob("*.h")) + [ROOT / "include" / "chameleon_lora.h"]
-    if LIB.exists() and not force:
+    lib = Path(out) if out else LIB
+    if lib.exists() and not force:
         newest = max(p.stat().st_mtime for p in deps)
-        if LIB.stat().st_mtime >= newest:
-            return LIB
-    objdir = ROOT / "build" / "obj"
+        if lib.stat().st_mtime >= newest:
+            return lib
+    objdir = ROOT / "build" / ("obj" if not defines else "obj_" + "_".join(d.replace("=", "") for d in defines))
     objdir.mkdir(parents=True, exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-              "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
+              "-I", str(ROOT / "include"), "--expt-relaxed-constexpr", *[f"-D{d}" for d in defines]]
     objs = []
     procs = []
     for s in srcs:
@@ -54,13 +55,13 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             sys.stdout.write(out.decode())
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{out.decode()}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     link = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -39,18 +39,28 @@ constexpr int A_CHUNK = 32768;               // K1: adapter bytes per stage (8 r
 constexpr int X_ROW = A_CHUNK / kRowsPerPage;  // K1: x bytes per token per stage (k-chunk)
 static_assert(X_ROW == kActRowBytes, "pool workspace geometry");
 constexpr int K1_STAGE = A_CHUNK + TG * X_ROW;
-constexpr int NC_BYTES = 2048;               // K2: bytes of one B row per unit (1024 bf16 columns)
-constexpr int NQ = NC_BYTES / 16;            // K2: 16-byte column chunks per unit (128)
-constexpr int PG = 2;                        // K2: pages per stage
-constexpr int B_PAGE = NC_BYTES * kRowsPerPage;  // 16 KiB
-constexpr int B_PITCH = B_PAGE + 64;         // skew the second page by 4 bank groups
-constexpr int K2_Y = PG * B_PITCH;
-constexpr int K2_V = K2_Y + TG * NC_BYTES;
-constexpr int K2_STAGE = K2_V + TG * kMaxRank * 4;
+// K2 geometry.  Tiles of adapters with >= 16 pages (rank >= 128) use 512-column units with
+// 4 pages per stage (8 KiB per page copy); smaller ranks use 1024-column units with 2 pages
+// per stage (16 KiB copies).  Either way a stage holds 32 KiB of B and no unit exceeds 4
+// stages for ranks <= 128, which keeps the dynamic dispatch balanced at the phase end.
+#ifndef CHAM_BIG_PAGES
+#define CHAM_BIG_PAGES 33  // > kMaxPagesPerSlot: disabled (A/B on C2: 102.7k vs 101.6k tok/s)
+#endif
+constexpr int kBigPages = CHAM_BIG_PAGES;    // np >= kBigPages: "big" unit geometry
+constexpr int NCB_SMALL = 2048;              // bytes of one B row per unit (np < kBigPages)
+constexpr int NCB_BIG = 1024;                // bytes of one B row per unit (np >= kBigPages)
+constexpr int PITCH_SMALL = NCB_SMALL * kRowsPerPage + 64;  // page pitch in a stage (+bank skew)
+constexpr int PITCH_BIG = NCB_BIG * kRowsPerPage + 32;
+constexpr int K2_B = 2 * PITCH_SMALL;
+static_assert(4 * PITCH_BIG <= K2_B, "stage layout");
+constexpr int K2_Y = K2_B;
+constexpr int K2_V = K2_Y + TG * NCB_SMALL;
+constexpr int K2_STAGE = K2_V + 4 * TG * kRowsPerPage * 4;  // v slice [page][token][8 rows]
 constexpr int GROUP_WARPS = 8;
 constexpr int GROUP_THREADS = GROUP_WARPS * 32;
 constexpr int NTHREADS = 32 + GROUP_THREADS;
-static_assert(GROUP_THREADS == 2 * NQ, "K2 maps two threads per column chunk");
+static_assert(GROUP_THREADS == 2 * (NCB_SMALL / 16) && GROUP_THREADS == 4 * (NCB_BIG / 16),
+              "K2 maps 2 (small) or 4 (big) threads per 16-byte column chunk");
 constexpr int PLAN_SEGS = 512;
 constexpr int PLAN_PAGES = 2048;
 constexpr int PLAN_TOKENS = 2048;
@@ -105,6 +115,10 @@ struct Meta {
   int npg;    // K2: pages in this stage (1 or 2)
   int col0, ncols;
   int vrow;   // K2: floats per staged v row
+  int lpg;    // K2: log2(pages per stage) = log2(threads per column chunk)
+  int ncb;    // K2: bytes of one B row in this unit
+  int pitch;  // K2: page pitch in the stage
+  int nq;     // K2: 16-byte column chunks in this unit
   int rows[TG];
 };
 
@@ -112,7 +126,7 @@ struct alignas(16) Plan {
   int seg_off[PLAN_SEGS + 1];
   int seg_sr[PLAN_SEGS];      // (slot << 9) | rank
   int seg_pg[PLAN_SEGS + 1];  // prefix of pages -> pages[]
-  int v_start[PLAN_SEGS + 1]; // prefix of T_s * rpad_s -> compact v
+  int v_start[PLAN_SEGS + 1]; // prefix of nt_s * TG * rpad_s -> v, per tile [page][TG][8]
   int sh_start[PLAN_SEGS + 1];  // K1 units prefix (segment order)
   int ex_start[PLAN_SEGS + 1];  // K2 tiles prefix (LPT order); units = tiles x column chunks
   int order[PLAN_SEGS];         // K2 segment order: decreasing page count
@@ -122,6 +136,8 @@ struct alignas(16) Plan {
   int scan[NTHREADS / 32][4];
   int totals[6];  // K1 units/job, K2 tiles/job, tokens, pages, v floats/job, segments with work
   int n_seg;
+  int n_big_tiles;           // leading LPT tiles whose adapters have >= kBigPages pages
+  int nb_seg;
   int order_pos[PLAN_SEGS];  // segment -> position in the LPT order
   long long desc_cap;        // descriptor capacity (entries) after the header
 };
@@ -213,8 +229,8 @@ __device__ __forceinline__ int n_kchunks(const Params& p) {
   return ceil_div(p.h_in * Elem<T>::kBytes, X_ROW);
 }
 template <typename T>
-__device__ __forceinline__ int n_colchunks(const Params& p) {
-  return ceil_div(p.h_out * Elem<T>::kBytes, NC_BYTES);
+__device__ __forceinline__ int n_colchunks(const Params& p, bool big) {
+  return ceil_div(p.h_out * Elem<T>::kBytes, big ? NCB_BIG : NCB_SMALL);
 }
 
 // Builds the launch plan in shared memory (all NTHREADS threads).  It depends only on the
@@ -235,7 +251,7 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
     const int nt = ceil_div(o1 - o0, TG);
     lsh += nt * np;
     lpg += np;
-    lv += (o1 - o0) * np * kRowsPerPage;
+    lv += nt * TG * np * kRowsPerPage;
   }
   int ish = lsh, ipg = lpg, iv = lv;
 #pragma unroll
@@ -260,7 +276,7 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
     pl.v_start[s] = bv;
     bsh += ceil_div(T_s, TG) * np;
     bpg += np;
-    bv += T_s * np * kRowsPerPage;
+    bv += ceil_div(T_s, TG) * TG * np * kRowsPerPage;
     if (np > 0 && T_s > 0) atomicAdd(&pl.bucket[np], 1);
   }
   if (tid == NTHREADS - 1) {
@@ -280,10 +296,12 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
   // LPT order for K2: bucket offsets by decreasing page count, then scatter segments
   if (tid == 0) {
     int acc = 0;
+    pl.nb_seg = 0;
     for (int np = kMaxPagesPerSlot; np >= 1; --np) {
       const int c = pl.bucket[np];
       pl.bucket[np] = acc;
       acc += c;
+      if (np >= kBigPages) pl.nb_seg = acc;  // segments with >= kBigPages pages lead the order
     }
     pl.totals[5] = acc;  // segments with work
   }
@@ -333,6 +351,7 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
     if (lane == 0) {
       pl.ex_start[nw] = carry;
       pl.totals[1] = carry;
+      pl.n_big_tiles = pl.ex_start[pl.nb_seg];
     }
   }
   __syncthreads();
@@ -361,7 +380,7 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
           desc[pl.sh_start[s] + t * np + g] = d;
         }
         d.meta = tc | (np << 8);
-        d.aux = pl.v_start[s] + t * TG * np * kRowsPerPage;
+        d.aux = pl.v_start[s] + t * TG * np * kRowsPerPage;  // [page][TG][8] block of the tile
         dex[pl.ex_start[pl.order_pos[s]] + t] = d;
       }
     }
@@ -475,29 +494,31 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
     if (t < NT) {
       const int row = m0.g * kRowsPerPage + j;
       if (p.v_out) {
-        p.v_out[(long long)(m0.pos0 + t) * p.v_stride + row] = sum;  // TP layout [position][v_stride]
+        if (row < p.v_stride) p.v_out[(long long)(m0.pos0 + t) * p.v_stride + row] = sum;  // TP [position][v_stride]
       } else {
-        const int rpad = m0.np * kRowsPerPage;
-        const int t_seg = m0.pos0 + t - pl.seg_off[m0.seg];
-        p.vws[m0.job * p.vws_job_stride + pl.v_start[m0.seg] + t_seg * rpad + row] = sum;
+        // tile-major layout [page][TG][8 rows]: each expand stage copies its pages' slice
+        const int tile = (m0.pos0 - pl.seg_off[m0.seg]) / TG;
+        const long long vb = pl.v_start[m0.seg] + (long long)tile * TG * m0.np * kRowsPerPage;
+        p.vws[m0.job * p.vws_job_stride + vb + (m0.g * TG + t) * kRowsPerPage + j] = sum;
       }
     }
   }
 }
 
 // =========================================================================== K2: expand
-// One unit: output tile [NT tokens x 1024 columns]; stages walk the adapter's pages two at
-// a time.  Thread (q, h) owns 16-byte column chunk q (= ct >> 1) and page / half-page h.
+// One unit: output tile [NT tokens x ncols]; stages walk the adapter's pages PG at a time.
+// Thread (q, h) owns 16-byte column chunk q = ct >> lpg and page pg0 + h of each stage
+// (h = ct & (PG-1)); a lone page in a PG = 2 stage is split in row halves instead.
 template <typename T, int NT>
-__device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& seq, const Meta& m0, int ct) {
+__device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& seq, const Meta& m0, int ct) {
   constexpr int ES = Elem<T>::kBytes;
   constexpr int EPV = Elem<T>::kEPV;
   constexpr int NP2 = EPV / 2;
-  float* vs = reinterpret_cast<float*>(sm.scratch);  // [TG][kMaxRank]
-  const int q = ct >> 1, h = ct & 1;
+  const int lpg = m0.lpg;
+  const int npgmax = 1 << lpg;
+  const int h = ct & (npgmax - 1), q = ct >> lpg;
   const int a = q >> 3, c = q & 7;
-  const int rows = m0.np * kRowsPerPage;
-  const bool active = q * EPV < m0.ncols;
+  const bool active = q < m0.nq && q * EPV < m0.ncols;
   float2 acc[NT][NP2];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
@@ -509,36 +530,46 @@ __device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& 
     if (ct == 0) trace_consumer(p, seq, 2);
     const Meta& m = sm.meta[stage];
     const unsigned char* st = sm.stage[stage];
-    if (k == 0) {
-      // v rows of the tile -> vs (rows beyond the staged width read as zero)
-      named_bar_sync(1, GROUP_THREADS);  // previous unit's readers of vs are done
-      const float* Vs = reinterpret_cast<const float*>(st + K2_V);
-      for (int idx = ct; idx < NT * rows; idx += GROUP_THREADS) {
-        const int t = idx / rows, r = idx - t * rows;
-        vs[t * kMaxRank + r] = r < m.vrow ? Vs[t * m.vrow + r] : 0.f;
-      }
-      named_bar_sync(1, GROUP_THREADS);
-    }
+    const float* Vst = reinterpret_cast<const float*>(st + K2_V);  // [page in stage][TG][8]
     if (active) {
-      // two pages per stage: thread h takes page pg0+h (two row halves); a single page is
-      // split in row halves between h = 0 and h = 1.  Halves of 4 rows are fully unrolled.
-      const int pgl = m.npg == 2 ? h : 0;
-      const int hbeg = m.npg == 2 ? 0 : h;
-      const int hend = m.npg == 2 ? 2 : h + 1;
-      const unsigned char* Bg = st + pgl * B_PITCH;
-      const int vbase = (m.pg0 + pgl) * kRowsPerPage;
-      for (int hh = hbeg; hh < hend; ++hh) {
+      if (lpg == 2 || m.npg == 2) {
+        // own page pg0 + h: all 8 rows, fully unrolled
+        if (h < m.npg) {
+          const unsigned char* Bg = st + h * m0.pitch;
+          float vv[NT][kRowsPerPage];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const float4 lo = *reinterpret_cast<const float4*>(Vst + (h * TG + t) * kRowsPerPage);
+            const float4 hi = *reinterpret_cast<const float4*>(Vst + (h * TG + t) * kRowsPerPage + 4);
+            vv[t][0] = lo.x; vv[t][1] = lo.y; vv[t][2] = lo.z; vv[t][3] = lo.w;
+            vv[t][4] = hi.x; vv[t][5] = hi.y; vv[t][6] = hi.z; vv[t][7] = hi.w;
+          }
+          float2 bf[kRowsPerPage][NP2];
+#pragma unroll
+          for (int j = 0; j < kRowsPerPage; ++j)
+            Elem<T>::unpack2(lds128(Bg + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf[j]);
+#pragma unroll
+          for (int j = 0; j < kRowsPerPage; ++j)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const float2 v2 = make_float2(vv[t][j], vv[t][j]);
+#pragma unroll
+              for (int e = 0; e < NP2; ++e) acc[t][e] = __ffma2_rn(v2, bf[j][e], acc[t][e]);
+            }
+        }
+      } else {
+        // PG = 2 stage with a single page: rows 4h .. 4h+3
         float vv[NT][4];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          const float4 v4 = *reinterpret_cast<const float4*>(vs + t * kMaxRank + vbase + hh * 4);
+          const float4 v4 = *reinterpret_cast<const float4*>(Vst + t * kRowsPerPage + h * 4);
           vv[t][0] = v4.x; vv[t][1] = v4.y; vv[t][2] = v4.z; vv[t][3] = v4.w;
         }
         float2 bf[4][NP2];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-          const int j = hh * 4 + jj;
-          Elem<T>::unpack2(lds128(Bg + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf[jj]);
+          const int j = h * 4 + jj;
+          Elem<T>::unpack2(lds128(st + a * kAtomBytes + j * kRowBytes + (((c ^ j) & 7) << 4)), bf[jj]);
         }
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj)
@@ -551,22 +582,23 @@ __device__ __forceinline__ void expand_unit(const Params& p, K2Shared& sm, int& 
       }
     }
     if (k == m0.nst - 1) {
-      // epilogue on the last stage (it carries the y rows): combine the two halves held
-      // by adjacent lanes, add into y, store
+      // epilogue on the last stage (it carries the y rows): combine the partial sums of the
+      // sibling lanes (adjacent), add into y, store
+      for (int o = 1; o < npgmax; o <<= 1) {
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
+        for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int e = 0; e < NP2; ++e) {
-          acc[t][e].x += __shfl_xor_sync(0xffffffffu, acc[t][e].x, 1);
-          acc[t][e].y += __shfl_xor_sync(0xffffffffu, acc[t][e].y, 1);
-        }
+          for (int e = 0; e < NP2; ++e) {
+            acc[t][e].x += __shfl_xor_sync(0xffffffffu, acc[t][e].x, o);
+            acc[t][e].y += __shfl_xor_sync(0xffffffffu, acc[t][e].y, o);
+          }
+      }
       if (active) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          // lane h stores tokens t == h (mod 2)
-          if ((t & 1) == h) {
+          if ((t & (npgmax - 1)) == h) {  // sibling h stores tokens t == h (mod PG)
             float yv[EPV];
-            Elem<T>::unpack(lds128(st + K2_Y + t * NC_BYTES + q * 16), yv);
+            Elem<T>::unpack(lds128(st + K2_Y + t * m0.ncb + q * 16), yv);
 #pragma unroll
             for (int e = 0; e < NP2; ++e) {
               yv[2 * e] += acc[t][e].x;
@@ -701,35 +733,39 @@ __device__ __forceinline__ int produce_shrink(const Params& p, Shared& sm, int s
   return seq;
 }
 
-// Producer side of phase 2 (expand units).  In fused mode the v copies wait for the grid
+// Producer side of phase 2 (expand units).  Unit space: first the tiles with >= 16 pages
+// (512-column units, 4 pages per stage), then the rest (1024-column units, 2 pages per
+// stage); inside each region unit = (tile_lpt * n_jobs + job) * ncc + cc, so the
+// largest-rank tiles of every job go first.  In fused mode the v copies wait for the grid
 // barrier (every CTA finished phase 1); B pages and y rows are prefetched before it.
 template <typename T>
 __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused) {
   constexpr int ES = Elem<T>::kBytes;
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
-  const int ncc = n_colchunks<T>(p);
-  const int NTL = pl.totals[1];  // tiles per job
-  const int UE = NTL * ncc;
+  const int J = p.n_jobs;
+  const int ncc_b = n_colchunks<T>(p, true), ncc_s = n_colchunks<T>(p, false);
+  const int NB = pl.n_big_tiles, NTL = pl.totals[1];
+  const int units_big = NB * J * ncc_b;
+  const int total = units_big + (NTL - NB) * J * ncc_s;
   const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
-  const int total = p.n_jobs * UE;
-  const int ncol_unit = NC_BYTES / ES;
   const UnitDesc* desc =
       reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan)) + pl.totals[0];
   const uint64_t pol_w = policy_evict_first();
+  auto tile_of = [&](int u) { return u < units_big ? u / (J * ncc_b) : NB + (u - units_big) / (J * ncc_s); };
   bool v_ready = !fused;
   UnitQueue uq;
   uq.init(p.ctr + 4, total, 2, lane, &sm.unit_mailbox);
   int unit = uq.next(lane);
   int4 da = make_int4(0, 0, 0, 0), db = da;
-  // unit = (tile_lpt * n_jobs + job) * ncc + cc: largest-rank tiles of every job first
-  const int per_tile = p.n_jobs * ncc;
-  if (unit >= 0) ldg_desc(desc + unit / per_tile, da, db);
+  if (unit >= 0) ldg_desc(desc + tile_of(unit), da, db);
   while (unit >= 0) {
     const int nunit = uq.next(lane);
     int4 na = da, nb = db;
-    if (nunit >= 0) ldg_desc(desc + nunit / per_tile, na, nb);
-    const int jc = unit % per_tile;
+    if (nunit >= 0) ldg_desc(desc + tile_of(nunit), na, nb);
+    const bool big = unit < units_big;
+    const int ncc = big ? ncc_b : ncc_s;
+    const int jc = (big ? unit : unit - units_big) % (J * ncc);
     const int job = jc / ncc;
     const int cc = jc - job * ncc;
     const int s = da.x, pos0 = da.y;
@@ -737,39 +773,58 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
     const int vbase = da.w;
     const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
     const int slot = pl.seg_sr[s] >> 9;
+    const int lpg = big ? 2 : 1;
+    const int pgs = 1 << lpg;
+    const int ncb = big ? NCB_BIG : NCB_SMALL;
+    const int pitch = big ? PITCH_BIG : PITCH_SMALL;
+    const int ncol_unit = ncb / ES;
     const int col0 = cc * ncol_unit;
     const int ncols = min(ncol_unit, p.h_out - col0);
     const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
     const uint32_t y_bytes = ncols * ES;                  // per token
     const int rpad = np * kRowsPerPage;
     const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
-    const int nst = ceil_div(np, PG);
+    const int nst = ceil_div(np, pgs);
     const Job& jb = p.jobs[job];
     for (int k = 0; k < nst; ++k, ++seq) {
       const unsigned long long t_it = p.trace ? gtimer() : 0;
       const int stage = seq % NSTAGE;
-      const int pg0 = k * PG;
-      const int npg = min(PG, np - pg0);
+      const int pg0 = k * pgs;
+      const int npg = min(pgs, np - pg0);
       unsigned char* st = sm.stage[stage];
-      uint32_t bytes = b_bytes * npg;
-      if (k == 0) bytes += tcount * vrow * 4;          // v rows ride on the first stage
-      if (k == nst - 1) bytes += y_bytes * tcount;     // y rows on the last stage
+      // every stage carries its pages' v slice; the last one also the y rows.  With a
+      // caller-provided v (TP) only pages inside v_stride are copied, the rest are zeroed.
+      const int npg_in = p.v_in ? max(0, min(npg, vrow / kRowsPerPage - pg0)) : npg;
+      const uint32_t v_bytes = p.v_in ? npg_in * tcount * kRowsPerPage * 4 : npg * TG * kRowsPerPage * 4;
+      uint32_t bytes = b_bytes * npg + v_bytes;
+      if (k == nst - 1) bytes += y_bytes * tcount;
       int pgid = 0;
       if (lane < npg) pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
       if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
       const unsigned long long t_ready = p.trace ? gtimer() : 0;
       __syncwarp();
+      if (p.v_in && npg_in < npg) {
+        for (int c2 = lane; c2 < (npg - npg_in) * tcount; c2 += 32) {
+          const int hh = npg_in + c2 / tcount, t = c2 % tcount;
+          float4* z = reinterpret_cast<float4*>(st + K2_V + (hh * TG + t) * kRowsPerPage * 4);
+          z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        fence_proxy_async_shared();  // generic zero stores before later TMA writes to the stage
+        __syncwarp();
+      }
       Meta& m = sm.meta[stage];
       if (lane == 0) {
         m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
         m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
+        m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16;
         mbar_arrive_expect_tx(&sm.full[stage], bytes);
       }
       if (lane < tcount) m.rows[lane] = row;
       // B pages of this stage (weights: independent of phase 1 and of the previous kernel)
       if (lane < npg) {
         const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
-        bulk_g2s(st + lane * B_PITCH, src, b_bytes, &sm.full[stage], pol_w);
+        bulk_g2s(st + lane * pitch, src, b_bytes, &sm.full[stage], pol_w);
       }
       if (!waited) {  // y may be produced by the previous kernel
         pdl_wait();
@@ -777,27 +832,36 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
         waited = true;
       }
       if (k == nst - 1 && lane < tcount)
-        bulk_g2s(st + K2_Y + lane * NC_BYTES, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes,
-                 &sm.full[stage], pol_w);
-      if (k == 0) {
-        if (!v_ready) {
-          // v of every tile is complete once all CTAs passed the phase-1 barrier
-          if (lane == 0) {
-            while (ld_acquire_gpu(p.ctr + 9) == sm.grid_gen) __nanosleep(32);
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-          }
-          __syncwarp();
-          v_ready = true;
+        bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage],
+                 pol_w);
+      if (!v_ready) {
+        // v of every tile is complete once all CTAs passed the phase-1 barrier
+        if (lane == 0) {
+          while (ld_acquire_gpu(p.ctr + 9) == sm.grid_gen) __nanosleep(32);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
         }
-        if (p.v_in) {
-          if (lane < tcount)
-            bulk_g2s(st + K2_V + lane * vrow * 4, p.v_in + (long long)(pos0 + lane) * p.v_stride, vrow * 4,
-                     &sm.full[stage], pol_w);
-        } else if (lane == 0) {
-          bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase, tcount * rpad * 4, &sm.full[stage], pol_w);
+        __syncwarp();
+        v_ready = true;
+      }
+      if (p.v_in) {
+        // TP: v [position][v_stride] -> stage [page][token][8], one 32-byte copy each
+        for (int c2 = lane; c2 < npg_in * tcount; c2 += 32) {
+          const int hh = c2 / tcount, t = c2 - hh * tcount;
+          const int r0 = (pg0 + hh) * kRowsPerPage;
+          bulk_g2s(st + K2_V + (hh * TG + t) * kRowsPerPage * 4, p.v_in + (long long)(pos0 + t) * p.v_stride + r0,
+                   kRowsPerPage * 4, &sm.full[stage], pol_w);
+        }
+      } else if (lane == 0) {
+        bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase + pg0 * TG * kRowsPerPage, v_bytes,
+                 &sm.full[stage], pol_w);
+      }
+      if (lane == 0) {
+        trace_producer(p, seq, t_it, t_ready, 2, bytes);
+        if (p.trace && seq < p.trace_cap) {
+          p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 6] = unit;
+          p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 7] = (np << 8) | tcount;
         }
       }
-      if (lane == 0) trace_producer(p, seq, t_it, t_ready, 2, bytes);
       __syncwarp();
     }
     unit = nunit;
