@@ -112,6 +112,9 @@ CHAM_API int cham_debug_set_trace(cham_pool* pool, void* dev_buf, int items_per_
  * p the A/B pointers are at the running offsets of the previous (l,p) blocks. */
 CHAM_API int cham_pack_adapter_host(const cham_pool* pool, int rank, const void* a, const void* b,
                            void* out);
+/* Same packing from an explicit geometry (no pool, no GPU needed). */
+CHAM_API int cham_pack_adapter_host_geom(int n_layers, int n_proj, const int* h_in, const int* h_out,
+                                         int dtype, int rank, const void* a, const void* b, void* out);
 /* Device variant of the same packing (a, b, out in device memory). */
 CHAM_API int cham_pack_adapter_device(const cham_pool* pool, int rank, const void* a, const void* b,
                              void* out, void* stream);

@@ -56,6 +56,7 @@ SIGNATURES = {
     "cham_debug_set_trace": (c_int, [_P, _P, c_int]),
     "cham_pool_copy_out": (c_int, [_P, c_size_t, c_size_t, _P, _P]),
     "cham_pack_adapter_host": (c_int, [_P, c_int, _P, _P, _P]),
+    "cham_pack_adapter_host_geom": (c_int, [c_int, c_int, _IP, _IP, c_int, c_int, _P, _P, _P]),
     "cham_pack_adapter_device": (c_int, [_P, c_int, _P, _P, _P, _P]),
     "cham_build_segments": (c_int, [_P, _P, _P, c_int, _P, _P, _P, _P, _P, _P]),
     "cham_plan_bytes": (c_size_t, [_P]),

@@ -298,39 +298,52 @@ int cham_pool_copy_out(const cham_pool* pool, size_t offset, size_t bytes, void*
   return CHAM_OK;
 }
 
-int cham_pack_adapter_host(const cham_pool* pool, int rank, const void* a, const void* b, void* out) {
-  if (!pool || !a || !b || !out) return fail(CHAM_ERR_INVALID, "cham_pack_adapter_host: null argument");
-  if (rank <= 0 || rank > kMaxRank) return fail(CHAM_ERR_LIMIT, "cham_pack_adapter_host: bad rank");
-  const int es = pool->es;
+int cham_pack_adapter_host_geom(int n_layers, int n_proj, const int* h_in, const int* h_out, int dtype, int rank,
+                                const void* a, const void* b, void* out) {
+  if (!h_in || !h_out || !a || !b || !out || n_layers <= 0 || n_proj <= 0)
+    return fail(CHAM_ERR_INVALID, "cham_pack_adapter_host_geom: bad argument");
+  if (dtype != CHAM_F32 && dtype != CHAM_BF16) return fail(CHAM_ERR_INVALID, "cham_pack_adapter_host_geom: dtype");
+  if (rank <= 0 || rank > kMaxRank) return fail(CHAM_ERR_LIMIT, "cham_pack_adapter_host_geom: bad rank");
+  const int es = dtype == CHAM_F32 ? 4 : 2;
   const int atom_e = kRowBytes / es;
+  size_t page_bytes = 0;
+  for (int p = 0; p < n_proj; ++p) {
+    if (h_in[p] <= 0 || h_out[p] <= 0 || h_in[p] % atom_e || h_out[p] % atom_e)
+      return fail(CHAM_ERR_INVALID, "cham_pack_adapter_host_geom: h_in/h_out must be multiples of the atom width");
+    page_bytes += (size_t)kRowsPerPage * (h_in[p] + h_out[p]) * es;
+  }
+  page_bytes *= n_layers;
   const int np = (rank + kRowsPerPage - 1) / kRowsPerPage;
   const char* ca = static_cast<const char*>(a);
   const char* cb = static_cast<const char*>(b);
   char* co = static_cast<char*>(out);
-  std::memset(co, 0, (size_t)np * pool->page_bytes);
-  size_t asrc = 0, bsrc = 0;
-  for (int l = 0; l < pool->n_layers; ++l)
-    for (int p = 0; p < pool->n_proj; ++p) {
-      const int lp = l * pool->n_proj + p;
-      const int hin = pool->h_in[p], hout = pool->h_out[p];
+  std::memset(co, 0, (size_t)np * page_bytes);
+  size_t off = 0, asrc = 0, bsrc = 0;
+  for (int l = 0; l < n_layers; ++l)
+    for (int p = 0; p < n_proj; ++p) {
+      const int hin = h_in[p], hout = h_out[p];
+      const size_t aoff = off, boff = off + (size_t)kRowsPerPage * hin * es;
+      off = boff + (size_t)kRowsPerPage * hout * es;
       for (int r = 0; r < rank; ++r) {
         const int page = r / kRowsPerPage, j = r % kRowsPerPage;
-        char* pg = co + (size_t)page * pool->page_bytes;
-        for (int k = 0; k < hin; ++k) {
-          const int atom = k / atom_e, e = k % atom_e;
-          std::memcpy(pg + pool->a_off[lp] + (size_t)atom * kAtomBytes + atom_offset(j, e, es),
+        char* pg = co + (size_t)page * page_bytes;
+        for (int k = 0; k < hin; ++k)
+          std::memcpy(pg + aoff + (size_t)(k / atom_e) * kAtomBytes + atom_offset(j, k % atom_e, es),
                       ca + asrc + ((size_t)k * rank + r) * es, es);
-        }
-        for (int n = 0; n < hout; ++n) {
-          const int atom = n / atom_e, e = n % atom_e;
-          std::memcpy(pg + pool->b_off[lp] + (size_t)atom * kAtomBytes + atom_offset(j, e, es),
+        for (int n = 0; n < hout; ++n)
+          std::memcpy(pg + boff + (size_t)(n / atom_e) * kAtomBytes + atom_offset(j, n % atom_e, es),
                       cb + bsrc + ((size_t)r * hout + n) * es, es);
-        }
       }
       asrc += (size_t)hin * rank * es;
       bsrc += (size_t)rank * hout * es;
     }
   return CHAM_OK;
+}
+
+int cham_pack_adapter_host(const cham_pool* pool, int rank, const void* a, const void* b, void* out) {
+  if (!pool) return fail(CHAM_ERR_INVALID, "cham_pack_adapter_host: null pool");
+  return cham_pack_adapter_host_geom(pool->n_layers, pool->n_proj, pool->h_in.data(), pool->h_out.data(),
+                                     pool->dtype, rank, a, b, out);
 }
 
 int cham_pack_adapter_device(const cham_pool* pool, int rank, const void* a, const void* b, void* out,

@@ -121,8 +121,8 @@ class LoraStepExecutor:
                                  layer=layer, projs=projs, stream=stream)
 
     def launches_per_step(self) -> int:
-        """Kernels per step: segment builder + plan + (shrink, expand) per (layer, group)."""
-        return 2 + 2 * self.pool.n_layers * len(self.proj_groups)
+        """Kernels per step: segment builder + plan + one fused apply per (layer, group)."""
+        return 2 + self.pool.n_layers * len(self.proj_groups)
 
     def run(self, xs_per_layer, ys_per_layer, stream=None) -> None:
         """K4 + every (layer, group) apply, on `stream`."""

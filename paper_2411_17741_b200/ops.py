@@ -164,15 +164,25 @@ def lora_apply_multi(xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], tab
          _stream_ptr(stream))
 
 
+def _check_v(v: torch.Tensor) -> None:
+    """v: fp32 [positions, cols] with unit column stride; the row stride (a multiple of 4
+    floats, 16-byte aligned base) is passed as v_stride, so a column slice of a wider
+    buffer (the fused q/k/v operand of one all-reduce) is accepted.  The kernels write and
+    read ranks up to the segment's padded rank: cols must cover it."""
+    if v.dtype != torch.float32 or v.dim() != 2 or v.stride(1) != 1:
+        raise ValueError("v must be an fp32 [positions, cols] tensor with unit column stride")
+    if v.stride(0) % 4 or v.data_ptr() % 16:
+        raise ValueError("v rows must be 16-byte aligned (row stride a multiple of 4 floats)")
+
+
 def lora_shrink(x: torch.Tensor, v: torch.Tensor, slot_ids, seg_offsets, ranks, *, pool: AdapterPool,
                 layer: int, proj: int, perm=None, n_seg: Optional[int] = None, plan=None,
                 stream=None) -> torch.Tensor:
     """v[k, :r] = x[perm[k]] . A_slot (fp32 [n_positions, v_stride]); the TP all-reduce operand."""
     _check_act(x, pool, pool.h_in[proj], "x")
-    if v.dtype != torch.float32 or v.dim() != 2 or not v.is_contiguous():
-        raise ValueError("v must be a contiguous fp32 [positions, v_stride] tensor")
+    _check_v(v)
     ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
-    call("cham_lora_shrink", pool.handle, int(layer), int(proj), x.data_ptr(), v.data_ptr(), int(v.shape[1]),
+    call("cham_lora_shrink", pool.handle, int(layer), int(proj), x.data_ptr(), v.data_ptr(), int(v.stride(0)),
          int(x.shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
          ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))
     return v
@@ -183,10 +193,9 @@ def lora_expand(v: torch.Tensor, y: torch.Tensor, slot_ids, seg_offsets, ranks, 
                 stream=None) -> torch.Tensor:
     """y[perm[k]] += v[k, :r] . B_slot (in place)."""
     _check_act(y, pool, pool.h_out[proj], "y")
-    if v.dtype != torch.float32 or v.dim() != 2 or not v.is_contiguous():
-        raise ValueError("v must be a contiguous fp32 [positions, v_stride] tensor")
+    _check_v(v)
     ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
-    call("cham_lora_expand", pool.handle, int(layer), int(proj), v.data_ptr(), int(v.shape[1]), y.data_ptr(),
+    call("cham_lora_expand", pool.handle, int(layer), int(proj), v.data_ptr(), int(v.stride(0)), y.data_ptr(),
          int(y.shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
          ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))
     return y

@@ -45,9 +45,19 @@ def zipf_batch(seed: int, n_tokens: int = 256, num_adapters: int = 1000, rank_se
 
 def prefill_batch(seed: int, n_segments: int = 64, tokens_per_segment: int = 64, num_adapters: int = 100,
                   rank_set=DEFAULT_RANK_SET):
-    """C3: n_segments prefill requests of tokens_per_segment tokens; ranks by the s=1 power law."""
+    """C3: n_segments prefill requests of tokens_per_segment tokens, one distinct adapter each
+    (BASELINE.json C3: 64 segments / 64 adapters).  Ranks are drawn directly with the s=1
+    power law from default_rng(seed) (seed 0: sum of ranks 1,864); the j-th
+    adapter of rank r is `r{r}-{j}`."""
+    ranks = sorted(rank_set)
     rng = np.random.default_rng(seed)
-    ids = [assign_adapter(rng, num_adapters, rank_set) for _ in range(n_segments)]
+    draws = rng.choice(len(ranks), n_segments, p=rank_probabilities(rank_set))
+    count: dict[int, int] = {}
+    ids = []
+    for i in draws:
+        r = ranks[int(i)]
+        ids.append(f"r{r}-{count.get(r, 0)}")
+        count[r] = count.get(r, 0) + 1
     return ids, [tokens_per_segment] * n_segments
 
 
