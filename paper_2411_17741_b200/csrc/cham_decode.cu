@@ -33,6 +33,10 @@
 namespace cham {
 namespace decode {
 
+#ifndef CHAM_EXP_NOCOMPUTE
+#define CHAM_EXP_NOCOMPUTE 0  // experiment builds only: consumers skip the math (data-movement ceiling)
+#endif
+constexpr bool kNoCompute = CHAM_EXP_NOCOMPUTE != 0;
 constexpr int TG = 4;                        // tokens per tile
 constexpr int NSTAGE = 4;
 constexpr int A_CHUNK = 32768;               // K1: adapter bytes per stage (8 rows x 4 KiB)
@@ -458,7 +462,7 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
     const unsigned char* st = sm.stage[stage];
     const int kbytes = min(X_ROW, p.h_in * ES - m.kc * X_ROW);
     const unsigned char* X = st + A_CHUNK;
-    for (int q = ct; q < (kbytes >> 4); q += GROUP_THREADS) {
+    for (int q = ct; q < (kNoCompute ? 0 : kbytes >> 4); q += GROUP_THREADS) {
       const int a = q >> 3, c = q & 7;
       float2 xf[NT][NP2];
 #pragma unroll
@@ -531,7 +535,7 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
     const Meta& m = sm.meta[stage];
     const unsigned char* st = sm.stage[stage];
     const float* Vst = reinterpret_cast<const float*>(st + K2_V);  // [page in stage][TG][8]
-    if (active) {
+    if (active && !kNoCompute) {
       if (lpg == 2 || m.npg == 2) {
         // own page pg0 + h: all 8 rows, fully unrolled
         if (h < m.npg) {

@@ -115,7 +115,7 @@ def main():
             lora_apply_table(xs[1], ys[3], ex.table, pool=pool, layer=7, proj=3)
         torch.cuda.synchronize()
         tr = buf.cpu().numpy()[0]
-        np.save(out / f"trace_{name}.npy", tr)
+        np.save(out / f"trace_{name}{os.environ.get('TRACE_TAG', '')}.npy", tr)
         analyze(tr, f"{name} fused kernel")
         valid = tr[:, :, 0] > 0
         t0 = tr[:, :, 0][valid].min()

@@ -235,3 +235,128 @@ def test_prebuilt_plan_matches_in_kernel_plan():
         assert torch.equal(a_, b_)
     assert torch.equal(yb[1], yc)
     pool.close()
+
+
+def test_tp2_70b_shards_through_strided_v():
+    """C5 at 70B dims, TP=2 emulated on one GPU: each rank's pool holds its shard (A on h_in,
+    B on h_out); shrink writes column slices of one fused q/k [n_pos, 2R] buffer, the
+    all-reduce is the sum of the two ranks' buffers, expand reads the slices back.  The
+    concatenated y shards must equal the unsharded oracle."""
+    from paper_2411_17741_b200.ops import lora_expand, lora_shrink
+    from paper_2411_17741_b200.tp import shard_bounds
+
+    rng = np.random.default_rng(5)
+    H_IN, H_OUT = [8192, 8192], [8192, 1024]  # q, k (GQA)
+    slot_ranks = {0: 64, 1: 64, 2: 64}
+    full = [make_adapters(rng, slot_ranks, H_IN[p], H_OUT[p], bf16=True) for p in range(2)]
+    req_slots = rng.integers(0, 3, 48).tolist()
+    req_slots[5] = -1
+    req_rank = [64 if s >= 0 else 0 for s in req_slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(req_slots, req_rank, [1] * 48)
+    x = bf16_round(rng.standard_normal((48, 8192)).astype(np.float32))
+    ys = [bf16_round(rng.standard_normal((48, H_OUT[p])).astype(np.float32)) for p in range(2)]
+    R, world = 64, 2
+    n_pos = int(seg_off[-1])
+    vs, pools, yd = [], [], []
+    for rank in range(world):
+        i0, i1 = shard_bounds(8192, world, rank)
+        h_out_l = [h // world for h in H_OUT]
+        pool = _pool(1, [4096, 4096], h_out_l, torch.bfloat16, 3 * 8)
+        sh = {}
+        for s in slot_ranks:
+            sh[s] = []
+            for p in range(2):
+                o0, o1 = shard_bounds(H_OUT[p], world, rank)
+                a, b = full[p][s]
+                sh[s].append((np.ascontiguousarray(a[i0:i1]), np.ascontiguousarray(b[:, o0:o1])))
+        _install(pool, sh, slot_ranks)
+        xd = torch.from_numpy(x[:, i0:i1].copy()).to("cuda", torch.bfloat16)
+        v = torch.zeros(n_pos, 2 * R, dtype=torch.float32, device="cuda")
+        for p in range(2):
+            lora_shrink(xd, v[:, p * R:(p + 1) * R], seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=p,
+                        perm=perm)
+        vs.append(v)
+        pools.append(pool)
+        yd.append([torch.from_numpy(ys[p][:, shard_bounds(H_OUT[p], world, rank)[0]:
+                                            shard_bounds(H_OUT[p], world, rank)[1]].copy()).to("cuda", torch.bfloat16)
+                   for p in range(2)])
+    v_sum = vs[0] + vs[1]  # the all-reduce
+    for rank in range(world):
+        for p in range(2):
+            lora_expand(v_sum[:, p * R:(p + 1) * R], yd[rank][p], seg_slot, seg_off, seg_rank, pool=pools[rank],
+                        layer=0, proj=p, perm=perm)
+    torch.cuda.synchronize()
+    for p in range(2):
+        got = torch.cat([yd[r][p] for r in range(world)], dim=1).float().cpu().numpy()
+        ref = lora_apply_ref(x, ys[p], perm, seg_off, seg_slot, seg_rank, full[p])
+        np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+    for pool in pools:
+        pool.close()
+
+
+def test_c3_prefill_shape_bf16():
+    """C3 shape at one (layer, proj): 64 segments x 64 tokens, 64 distinct adapters with
+    ranks from workload.prefill_batch(0)."""
+    from paper_2411_17741_b200.workload import prefill_batch, rank_of_id
+
+    ids, ntok = prefill_batch(0)
+    slot_ranks = {i: rank_of_id(a) for i, a in enumerate(ids)}
+    got, ref = _run_case(torch.bfloat16, 4096, 4096, slot_ranks, list(range(64)), ntok, seed=9)
+    np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_paged_cache_fills_evictions_and_page_reuse():
+    """Miniature C4: a Zipf stream through PagedAdapterCache with capacity for a fraction of
+    the catalog.  Misses evict, pages are reused, fills run on the side stream; every step's
+    lora_apply must match the oracle over the true adapter weights."""
+    from paper_2411_17741_b200.adapter_cache import PagedAdapterCache
+    from paper_2411_17741_b200.model import CacheConfig, make_adapter_spec
+    from paper_2411_17741_b200.ops import lora_apply
+    from paper_2411_17741_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(21)
+    H = 256
+    ranks = [8, 16, 32, 64, 128]
+    catalog = {f"r{ranks[i % 5]}-{i // 5}": make_adapter_spec(f"r{ranks[i % 5]}-{i // 5}", ranks[i % 5])
+               for i in range(25)}
+    ids = list(catalog)
+    weights = make_adapters(rng, {i: catalog[a].rank for i, a in enumerate(ids)}, H, H, bf16=True)
+    pool = AdapterPool(64, 1, [H], [H], dtype=torch.bfloat16, n_slots=len(ids), max_tokens=256)
+    store = {a: pool.pack_host([torch.from_numpy(weights[i][0])], [torch.from_numpy(weights[i][1])],
+                               catalog[a].rank) for i, a in enumerate(ids)}
+    cache = PagedAdapterCache(CacheConfig(), catalog, pool, host_store=store)
+    cache.set_capacity(64 * 32, set(), 0)  # 41% of the catalog's 4,960 tokens
+    p = np.array([(i + 1) ** -0.7 for i in range(len(ids))])
+    p /= p.sum()
+    now, evictions = 0, 0
+    for step in range(40):
+        now += 1000
+        batch = [ids[int(k)] for k in rng.choice(len(ids), 24, p=p)]
+        distinct = sorted(set(batch), key=batch.index)[:3]  # <= 1,536 pinned tokens
+        batch = [a for a in batch if a in distinct]
+        for a in distinct:
+            if not cache.acquire(a, now).hit:
+                e = cache.lookup(a)
+                if not e.loading:
+                    evictions += len(cache.evict_until(e.size_tokens, set(distinct), now))
+                    cache.begin_load(a, now)
+                cache.wait_ready([a])
+                torch.cuda.current_stream().synchronize()
+                cache.finish_load(a, now)
+                cache.take_ref(a, now)
+        slots = [cache.slot_of(a) for a in batch]
+        rks = [catalog[a].rank for a in batch]
+        perm, seg_off, seg_slot, seg_rank = build_segments_ref(slots, rks, [1] * len(batch))
+        x = bf16_round(rng.standard_normal((len(batch), H)).astype(np.float32))
+        y0 = bf16_round(rng.standard_normal((len(batch), H)).astype(np.float32))
+        yd = torch.from_numpy(y0).to("cuda", torch.bfloat16)
+        lora_apply(torch.from_numpy(x).to("cuda", torch.bfloat16), yd, seg_slot, seg_off, seg_rank, pool=pool,
+                   layer=0, proj=0, perm=perm)
+        torch.cuda.synchronize()
+        ref = lora_apply_ref(x, y0, perm, seg_off, seg_slot, seg_rank, weights)
+        np.testing.assert_allclose(yd.float().cpu().numpy(), ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+        for a in distinct:
+            cache.release(a, now)
+    assert evictions > 0 and cache.fill_count > len(set(ids)) // 2
+    assert cache.used_tokens == cache.resident_tokens_recount()
+    pool.close()
