@@ -111,7 +111,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU path
-def cpu_oracle_sample(batch_ids, seconds: float = 12.0):
+def cpu_oracle_sample(batch_ids, seconds: float = 12.0, ntok=None):
     """numpy fp32 restatement (oracle/lora_ref.py) of one (layer, proj) apply of the batch,
     repeated for ~`seconds`; returns (seconds per layer-proj, cores, sample description)."""
     from oracle.lora_ref import lora_apply_ref
@@ -128,9 +128,10 @@ def cpu_oracle_sample(batch_ids, seconds: float = 12.0):
                              (rng.standard_normal((r, H)) * 0.02).astype(np.float32))
     ranks = [rank_of_id(a) for a in batch_ids]
     slots = [slot[a] for a in batch_ids]
-    perm, off, sl, rk = build_segments_ref(slots, ranks, [1] * len(batch_ids))
-    x = rng.standard_normal((len(batch_ids), H)).astype(np.float32)
-    y = rng.standard_normal((len(batch_ids), H)).astype(np.float32)
+    ntok = [1] * len(batch_ids) if ntok is None else [int(t) for t in ntok]
+    perm, off, sl, rk = build_segments_ref(slots, ranks, ntok)
+    x = rng.standard_normal((sum(ntok), H)).astype(np.float32)
+    y = rng.standard_normal((sum(ntok), H)).astype(np.float32)
     n = 0
     t0 = time.perf_counter()
     while True:
@@ -140,7 +141,8 @@ def cpu_oracle_sample(batch_ids, seconds: float = 12.0):
             break
     dt = (time.perf_counter() - t0) / n
     cores = len(os.sched_getaffinity(0))
-    return dt, cores, f"{n} x one (layer,proj) apply of the C2 batch ({len(batch_ids)} tok, {len(uniq)} adapters), numpy fp32"
+    return dt, cores, (f"{n} x one (layer,proj) apply of the batch ({sum(ntok)} tok, {len(uniq)} adapters), "
+                       "numpy fp32")
 
 
 def run_reference(args, rank: int, world: int):
@@ -179,14 +181,24 @@ def run_ours(args, rank: int, world: int):
     from paper_2411_17741_b200.executor import LoraStepExecutor
     from paper_2411_17741_b200.model import build_catalog
     from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
-    from paper_2411_17741_b200.workload import decode_batch, rank_of_id
+    from paper_2411_17741_b200.workload import decode_batch, prefill_batch, rank_of_id
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    catalog = build_catalog(NUM_ADAPTERS)
-    ids = list(catalog)
+    if args.config == "c3":
+        # C3: 64 prefill segments x 64 tokens, one distinct adapter each (prefill_batch(seed=rank))
+        pids, pntok = prefill_batch(rank)
+        ids = list(dict.fromkeys(pids))
+        rank_of = {a: rank_of_id(a) for a in ids}
+        batch, ntok_list = pids, pntok
+    else:
+        catalog = build_catalog(NUM_ADAPTERS)
+        ids = list(catalog)
+        rank_of = {a: catalog[a].rank for a in ids}
+        batch = decode_batch(rank, T_DECODE, NUM_ADAPTERS)
+        ntok_list = [1] * len(batch)
     slot_of = {a: i for i, a in enumerate(ids)}
-    n_pages = sum(pages_for_rank(s.rank) for s in catalog.values())
+    n_pages = sum(pages_for_rank(rank_of[a]) for a in ids)
     pool = AdapterPool(n_pages, N_LAYERS, [H] * N_PROJ, [H] * N_PROJ, dtype=torch.bfloat16,
                        n_slots=len(ids), max_tokens=4096, device=dev)
     # synthetic random-init adapters: every page of every adapter gets N(0, 0.02) bf16 values
@@ -194,7 +206,7 @@ def run_ours(args, rank: int, world: int):
     gen.manual_seed(1234 + rank)
     page = 0
     for a in ids:
-        r = catalog[a].rank
+        r = rank_of[a]
         npg = pages_for_rank(r)
         pool.set_slot(slot_of[a], r, list(range(page, page + npg)))
         buf = (torch.randn(npg * pool.page_bytes // 2, generator=gen, device=dev) * 0.02).to(torch.bfloat16)
@@ -203,10 +215,9 @@ def run_ours(args, rank: int, world: int):
         del buf
     torch.cuda.synchronize(dev)
 
-    batch = decode_batch(rank, T_DECODE, NUM_ADAPTERS)
     req_slot = np.array([slot_of[a] for a in batch], dtype=np.int32)
-    req_rank = np.array([rank_of_id(a) for a in batch], dtype=np.int32)
-    req_ntok = np.ones(len(batch), dtype=np.int32)
+    req_rank = np.array([rank_of[a] for a in batch], dtype=np.int32)
+    req_ntok = np.array(ntok_list, dtype=np.int32)
 
     groups = [[0, 1, 2], [3]] if args.mode == "qkv" else [[0], [1], [2], [3]]
     ex = LoraStepExecutor(pool, max_requests=1024, max_tokens=4096, proj_groups=groups)
@@ -298,20 +309,27 @@ def run_ours(args, rank: int, world: int):
     bytes_step = (a_bytes + act_bytes) * lp
     adapter_bytes_step = a_bytes * lp
     flops_step = int(2 * sum(int(rk[i]) * int(off[i + 1] - off[i]) for i in range(len(sl))) * (H + H) * lp)
-    hbm_peak, _, peak_kind = peaks()
+    hbm_peak, bf16_peak, peak_kind = peaks()
     apply_launches = N_LAYERS * len(groups)
     achieved = bytes_step / (apply_ms * 1e-3) / 1e9
 
     if rank == 0:
         tokens_total = T * world
         value = tokens_total / (step_ms * 1e-3)
+        if args.config == "c3":
+            workload = ("C3: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers) prefill, 64 segments x 64 tokens over "
+                        "64 adapters with power-law ranks (prefill_batch seed = rank), tcgen05 path")
+            kernels = "prefill::shrink_kernel + prefill::expand_kernel (tcgen05, TMEM accumulators) per apply"
+        else:
+            workload = ("C2: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers), 100 adapters ranks 8-128, "
+                        "decode batch 256 tokens per GPU (assign_adapter seed = rank)")
+            kernels = "decode::lora_apply_kernel<bf16> (fused shrink -> grid barrier -> expand, PDL-chained)"
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers), 100 adapters ranks 8-128, "
-                                   "decode batch 256 tokens per GPU (assign_adapter seed = rank)",
-                       "global_batch": tokens_total, "seq_len": 1, "parallelism": f"replicas x{world}",
+            "config": {"workload": workload,
+                       "global_batch": tokens_total, "seq_len": int(req_ntok.max()), "parallelism": f"replicas x{world}",
                        "launch_mode": args.mode,
                        "l2": "inputs larger than L2: each step streams 8 GB of distinct adapter pages "
                              "(128 (layer,proj) blocks) through the 126 MB L2"},
@@ -319,20 +337,21 @@ def run_ours(args, rank: int, world: int):
             "adapter_read_frac_of_peak": adapter_bytes_step / (step_ms * 1e-3) / 1e9 / hbm_peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "kernel": "lora_shrink_kernel<bf16> + lora_expand_kernel<bf16> (PDL pair per apply)",
+                         "kernel": kernels,
                          "bytes_per_step": bytes_step, "launches_per_step": apply_launches,
                          "avg_launch_us": apply_ms * 1e3 / apply_launches,
                          "traffic": None},
             "flops_per_step": flops_step,
+            "tensor_frac_of_peak": flops_step / (apply_ms * 1e-3) / 1e12 / bf16_peak,
             "e2e": {"value": tokens_total / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": args.steps * ex.launches_per_step(),
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            t_lp, cores, sample = cpu_oracle_sample(batch, seconds=args.cpu_seconds)
+            t_lp, cores, sample = cpu_oracle_sample(batch, seconds=args.cpu_seconds, ntok=list(req_ntok))
             line["cpu_baseline"] = {"value": T / (t_lp * lp), "unit": "tokens/s", "cores": cores, "kind": "port",
-                                    "sample": sample + "; tokens/s = 256 / (128 x that)"}
+                                    "sample": sample + f"; tokens/s = {T} / (128 x that)"}
         print(json.dumps(line), flush=True)
     pool.close()
 
@@ -344,6 +363,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["qkv", "per-proj"], default="qkv")
+    ap.add_argument("--config", choices=["c2", "c3"], default="c2",
+                    help="c2 (default, the BASELINE metric's decode config) or c3 (prefill, tcgen05 path)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

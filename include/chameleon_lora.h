@@ -101,6 +101,17 @@ CHAM_API int cham_pool_fill_from_device(cham_pool* pool, int slot, const void* d
  * (host or device memory; synchronous on `stream`).  Introspection / tests. */
 CHAM_API int cham_pool_copy_out(const cham_pool* pool, size_t offset, size_t bytes, void* dst, void* stream);
 
+/* Routing of prefill-sized segments to the tcgen05 kernels (K3, bf16 pools whose h_in and
+ * h_out are multiples of 128).  A segment with >= min_tokens tokens and rank <= 128 runs on
+ * the tensor cores; every other segment runs on the decode GEMV kernel.  min_tokens <= 0
+ * disables the tcgen05 path.  min/max_segment_tokens are optional host hints about the
+ * segments of the steps that follow (0 / -1 = unknown): with max < min_tokens the tcgen05
+ * kernels are not launched, with min >= min_tokens the decode kernel is not launched.  Set
+ * the route before cham_build_plan and keep it for the step (the plan and the launches must
+ * agree).  Default: min_tokens = 64 (prefill_min_tokens of cham_limits), no hints. */
+CHAM_API int cham_pool_set_prefill_route(cham_pool* pool, int min_tokens, int min_segment_tokens,
+                                         int max_segment_tokens);
+
 /* Debug: record a per-item timeline of the decode kernel into `dev_buf`
  * (2 x [sm_count][items_per_cta][8] u64 — shrink kernel then expand kernel: producer issue
  * ns, kind<<32|bytes, consumer start ns, consumer end ns).  NULL disables.  Not for production use (adds global stores). */

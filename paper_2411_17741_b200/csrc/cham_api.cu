@@ -60,8 +60,6 @@ int cham_build_plan(cham_pool* pool, const int* perm, const int* seg_off, const 
   return build_plan_entry(pool, perm, seg_off, seg_slot, seg_rank, n_seg, n_seg_dev, plan, stream);
 }
 
-int cham_prefill_min_tokens_internal() { return 1 << 30; }
-
 size_t cham_plan_bytes_internal(const cham_pool* pool) { return plan_bytes(pool); }
 
 }  // extern "C"

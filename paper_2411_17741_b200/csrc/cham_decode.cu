@@ -31,6 +31,10 @@
 #include "cham_pool.h"
 
 namespace cham {
+int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
+                   void* const* ys, const int* perm, const int* seg_off, const int* seg_slot, const int* seg_rank,
+                   int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out, const float* v_in,
+                   int v_stride);
 namespace decode {
 
 #ifndef CHAM_EXP_NOCOMPUTE
@@ -106,6 +110,7 @@ struct Params {
   int trace_cap;
   const void* plan;           // Plan header + unit descriptors (cham_build_plan)
   long long desc_cap;
+  int prefill_thr;            // segments routed to the tcgen05 kernels (cham_prefill.cu) are skipped
 };
 
 // Per-stage record written by the producer, read by the consumers after the full barrier.
@@ -250,7 +255,9 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
     const int slot = p.seg_slot[s];
     const int rank = slot >= 0 ? min(p.seg_rank[s], kMaxRank) : 0;
     pl.seg_off[s] = o0;
-    pl.seg_sr[s] = slot >= 0 ? ((slot << 9) | rank) : 0;
+    // segments of the tcgen05 prefill path carry no decode work (rank 0 here)
+    const bool pre = is_prefill_segment(o1 - o0, rank, p.prefill_thr);
+    pl.seg_sr[s] = (slot >= 0 && !pre) ? ((slot << 9) | rank) : 0;
     const int np = ceil_div(rank, kRowsPerPage);
     const int nt = ceil_div(o1 - o0, TG);
     lsh += nt * np;
@@ -1045,6 +1052,7 @@ int build_plan_entry(cham_pool* pool, const int* perm, const int* seg_off, const
   prm.max_tokens = pool->max_tokens;
   prm.err = pool->d_ctr + 2;
   prm.desc_cap = plan_desc_capacity(pool->max_tokens);
+  prm.prefill_thr = prefill_route_thr(pool);
   build_plan_kernel<<<1, NTHREADS, sizeof(Plan), (cudaStream_t)stream>>>(prm, static_cast<Plan*>(plan));
   CHAM_CUDA(cudaGetLastError());
   return CHAM_OK;
@@ -1112,8 +1120,20 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
     plan = pool->d_plan;
   }
   prm.plan = plan;
-  if (pool->dtype == CHAM_BF16) return launch<__nv_bfloat16>(pool, prm, mode, (cudaStream_t)stream);
-  return launch<float>(pool, prm, mode, (cudaStream_t)stream);
+  prm.prefill_thr = prefill_route_thr(pool);
+  const bool pre = prm.prefill_thr < (1 << 30) && n_tokens >= prm.prefill_thr;
+  // with a host guarantee that every segment is prefill-sized, the decode kernel has no work
+  const bool dec = !pre || pool->route_min_seg < prm.prefill_thr;
+  int rc = CHAM_OK;
+  if (dec) {
+    rc = pool->dtype == CHAM_BF16 ? launch<__nv_bfloat16>(pool, prm, mode, (cudaStream_t)stream)
+                                  : launch<float>(pool, prm, mode, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  if (pre)
+    rc = prefill_launch(pool, layer, n_jobs, projs, xs, ys, perm, seg_off, seg_slot, seg_rank, n_seg, n_seg_dev,
+                        stream, mode, v_out, v_in, v_stride);
+  return rc;
 }
 
 }  // namespace cham

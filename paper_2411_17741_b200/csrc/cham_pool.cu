@@ -97,9 +97,7 @@ int cham_get_limits(cham_limits* out) {
   out->max_requests = kMaxRequests;
   out->rows_per_page = kRowsPerPage;
   out->tokens_per_tile = 4;
-  out->prefill_min_tokens = 1 << 30;  // set by the tcgen05 TU when compiled in
-  extern int cham_prefill_min_tokens_internal();
-  out->prefill_min_tokens = cham_prefill_min_tokens_internal();
+  out->prefill_min_tokens = kPrefillMinTokens;  // default of bf16 pools (cham_pool_set_prefill_route)
   return CHAM_OK;
 }
 
@@ -148,6 +146,10 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
       off += (size_t)kRowsPerPage * h_out[p] * es;
     }
   pool->page_bytes = off;
+  pool->prefill_ok = dtype == CHAM_BF16;
+  for (int p = 0; p < n_proj; ++p)
+    if (h_in[p] % 128 || h_out[p] % 128) pool->prefill_ok = false;
+  pool->prefill_min_tokens = pool->prefill_ok ? kPrefillMinTokens : 0;
   pool->vws_kc = (int)((hin_max * es + kActRowBytes - 1) / kActRowBytes);
   pool->slot_rank.assign(n_slots, 0);
   pool->slot_pages.assign((size_t)n_slots * kMaxPagesPerSlot, -1);
@@ -161,6 +163,7 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_ctr);
     cudaFree(pool->d_vws);
     cudaFree(pool->d_plan);
+    cudaFree(pool->d_pws);
     delete pool;
     cudaSetDevice(prev);
     return fail(code, msg);
@@ -184,6 +187,8 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     extern size_t cham_plan_bytes_internal(const cham_pool*);
     e = cudaMalloc(&pool->d_plan, cham_plan_bytes_internal(pool));
   }
+  if (e == cudaSuccess && pool->prefill_ok)
+    e = cudaMalloc(&pool->d_pws, sizeof(float) * (size_t)kMaxJobs * kPrefillMaxSplit * max_tokens * kPrefillMaxRank);
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);
@@ -204,7 +209,20 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_ctr);
   cudaFree(pool->d_vws);
   cudaFree(pool->d_plan);
+  cudaFree(pool->d_pws);
   delete pool;
+  return CHAM_OK;
+}
+
+int cham_pool_set_prefill_route(cham_pool* pool, int min_tokens, int min_segment_tokens,
+                                int max_segment_tokens) {
+  if (!pool) return fail(CHAM_ERR_INVALID, "cham_pool_set_prefill_route: null pool");
+  if (min_tokens > 0 && !pool->prefill_ok)
+    return fail(CHAM_ERR_UNSUPPORTED,
+                "cham_pool_set_prefill_route: the tcgen05 path needs a bf16 pool with h_in, h_out multiples of 128");
+  pool->prefill_min_tokens = min_tokens > 0 ? min_tokens : 0;
+  pool->route_min_seg = min_segment_tokens > 0 ? min_segment_tokens : 0;
+  pool->route_max_seg = max_segment_tokens >= 0 ? max_segment_tokens : (1 << 30);
   return CHAM_OK;
 }
 

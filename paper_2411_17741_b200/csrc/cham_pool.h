@@ -31,9 +31,31 @@ struct cham_pool {
   void* d_plan = nullptr;              // scratch plan for calls without a step-level plan
   unsigned long long* d_trace = nullptr;  // debug timeline buffer (caller-owned)
   int trace_cap = 0;
+  // tcgen05 prefill routing (cham_prefill.cu): segments with >= prefill_min_tokens tokens and
+  // rank <= kPrefillMaxRank run the tensor-core kernels; the decode plan skips them.
+  bool prefill_ok = false;             // bf16 pool, every h_in / h_out a multiple of 128
+  int prefill_min_tokens = 0;          // 0 = tcgen05 path disabled
+  int route_min_seg = 0;               // host hints about the next steps' segment lengths
+  int route_max_seg = 1 << 30;
+  float* d_pws = nullptr;              // prefill shrink partials [kMaxJobs][ks][max_tokens][128]
 };
 
 namespace cham {
+constexpr int kPrefillMinTokens = 64;  // default routing threshold (segment tokens)
+constexpr int kPrefillMaxRank = 128;   // largest rank on the tcgen05 path (TMEM / smem budget)
+constexpr int kPrefillMaxSplit = 8;    // shrink split-K factor bound (workspace sizing)
+
+// Threshold the plan and the launches use for this pool: segments with at least this many
+// tokens (and rank <= kPrefillMaxRank) go to the tcgen05 kernels.  INT_MAX = none.
+inline int prefill_route_thr(const cham_pool* pool) {
+  if (!pool->prefill_ok || pool->prefill_min_tokens <= 0) return 1 << 30;
+  if (pool->route_max_seg < pool->prefill_min_tokens) return 1 << 30;
+  return pool->prefill_min_tokens;
+}
+__host__ __device__ inline bool is_prefill_segment(int n_tok, int rank, int thr) {
+  return n_tok >= thr && rank > 0 && rank <= kPrefillMaxRank;
+}
+
 // Byte offset of element (row j, element e) inside a 1 KiB swizzled atom.
 __host__ __device__ inline uint32_t atom_offset(int j, int e, int es) {
   const int byte = e * es;

@@ -47,6 +47,25 @@ def batch_arrays(batch, slot_of: Callable[[str], int], rank_of: Callable[[str], 
             np.asarray(ntok, dtype=np.int32))
 
 
+def segment_token_bounds(req_slot, req_rank, req_ntok, max_rank: int = 128) -> tuple[int, int]:
+    """(min, max) tokens over the step's segments (one segment per distinct slot >= 0), the
+    routing hints of cham_pool_set_prefill_route.  A segment whose rank exceeds the tcgen05
+    path's limit forces min = 0 (it needs the decode kernel).  Vectorised, no per-request loop."""
+    slot = np.asarray(req_slot, dtype=np.int64)
+    ntok = np.asarray(req_ntok, dtype=np.int64)
+    rank = np.asarray(req_rank, dtype=np.int64)
+    m = slot >= 0
+    if not m.any():
+        return 0, 0
+    tok = np.bincount(slot[m], weights=ntok[m]).astype(np.int64)
+    present = np.bincount(slot[m]) > 0
+    seg = tok[present]
+    lo, hi = int(seg.min()), int(seg.max())
+    if (rank[m] > max_rank).any():
+        lo = 0
+    return lo, hi
+
+
 def adapter_units(batch, rank_of: Callable[[str], int]) -> int:
     """The reference's `adapter_units` of a step (engine.py:64-76), as an integer."""
     _, ranks, ntok = batch_arrays(batch, lambda a: 0, rank_of)
@@ -61,8 +80,17 @@ class LoraStepExecutor:
     """
 
     def __init__(self, pool: AdapterPool, max_requests: int = 4096, max_tokens: Optional[int] = None,
-                 proj_groups: Optional[Sequence[Sequence[int]]] = None, stream=None):
+                 proj_groups: Optional[Sequence[Sequence[int]]] = None, stream=None, prefill_min_tokens: int = 64,
+                 route_hints: bool = True):
         self.pool = pool
+        # tcgen05 routing: segments >= prefill_min_tokens (bf16 pools; 0 disables).  With
+        # route_hints the host passes each step's segment-length bounds, so only the kernel
+        # family with work is launched (set before the step's plan is built / captured).
+        self.prefill_min_tokens = int(prefill_min_tokens) if pool.dtype == torch.bfloat16 else 0
+        self.route_hints = route_hints
+        self.prefill_launched = False
+        self.decode_launched = True
+        pool.set_prefill_route(self.prefill_min_tokens)
         dev = pool.device
         self.max_requests = min(int(max_requests), _lib.limits().max_requests)
         self.max_tokens = int(max_tokens or pool.max_tokens)
@@ -99,6 +127,11 @@ class LoraStepExecutor:
         with torch.cuda.stream(s):
             self.req_dev[:, :n].copy_(self.req_host[:, :n], non_blocking=True)
         self.n_req = n
+        if self.route_hints:
+            lo, hi = segment_token_bounds(req_slot, req_rank, req_ntok)
+            self.pool.set_prefill_route(self.prefill_min_tokens, lo, hi)
+            self.prefill_launched = self.prefill_min_tokens > 0 and hi >= self.prefill_min_tokens
+            self.decode_launched = not self.prefill_launched or lo < self.prefill_min_tokens
         return total
 
     # -- device side (capturable) ------------------------------------------------------------
@@ -121,8 +154,10 @@ class LoraStepExecutor:
                                  layer=layer, projs=projs, stream=stream)
 
     def launches_per_step(self) -> int:
-        """Kernels per step: segment builder + plan + one fused apply per (layer, group)."""
-        return 2 + self.pool.n_layers * len(self.proj_groups)
+        """Kernels per step: segment builder + plan + per (layer, group) the decode kernel
+        and/or the two tcgen05 prefill kernels."""
+        per = (1 if self.decode_launched else 0) + (2 if self.prefill_launched else 0)
+        return 2 + self.pool.n_layers * len(self.proj_groups) * per
 
     def run(self, xs_per_layer, ys_per_layer, stream=None) -> None:
         """K4 + every (layer, group) apply, on `stream`."""

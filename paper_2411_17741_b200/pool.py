@@ -108,6 +108,16 @@ class AdapterPool:
         self.slot_rank[slot] = int(rank)
         self.slot_pages[slot] = pages
 
+    # -- routing -----------------------------------------------------------------------
+    def set_prefill_route(self, min_tokens: int = 64, min_segment_tokens: int = 0,
+                          max_segment_tokens: int = -1) -> None:
+        """Segments with >= min_tokens tokens (rank <= 128) run on the tcgen05 prefill kernels
+        (bf16 pools only); min_tokens <= 0 sends everything to the decode kernel.  The
+        segment-length hints (0 / -1 = unknown) let a launch skip the kernel family that has
+        no work; set them before the step's plan is built."""
+        call("cham_pool_set_prefill_route", self.handle, int(min_tokens), int(min_segment_tokens),
+             int(max_segment_tokens))
+
     # -- packing -----------------------------------------------------------------------
     def _flatten(self, a_list, b_list, rank: int, device):
         n_lp = self.n_layers * self.n_proj
