@@ -356,6 +356,151 @@ def run_ours(args, rank: int, world: int):
     pool.close()
 
 
+# --------------------------------------------------------------------------- C4: cache with misses
+def run_c4(args, rank: int, world: int):
+    """C4 replica: 1000-adapter Zipf(0.7) catalog, PagedAdapterCache at 10% of idle HBM, decode
+    batches of 256 requests (zipf draws seeded by replica rank and step).  A step = the
+    reference's admission path for every request (acquire; on a miss evict_until + begin_load
+    with the pinned fill on the side stream; finish_load + take_ref when the copy's event
+    completes — engine.py:491-532, 294-301), the step graph (K4 + plan + 64 applies) on the
+    compute stream gated on the fills, then release of every request's reference.  Timed by
+    wall clock around all steps (host decisions and PCIe fills included)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_17741_b200.adapter_cache import InsufficientEvictableMemory, PagedAdapterCache
+    from paper_2411_17741_b200.executor import LoraStepExecutor
+    from paper_2411_17741_b200.model import CacheConfig, make_adapter_spec, zipf_catalog
+    from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    ids, probs = zipf_catalog(1000)
+    catalog = {a: make_adapter_spec(a, int(a[1:].split("-")[0])) for a in ids}
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    page_bytes = N_LAYERS * N_PROJ * 8 * (H + H) * 2
+    n_pages = int(0.10 * free_b) // page_bytes
+    pool = AdapterPool(n_pages, N_LAYERS, [H] * N_PROJ, [H] * N_PROJ, dtype=torch.bfloat16, n_slots=len(ids),
+                       max_tokens=4096, device=dev)
+    # host repository: one pinned synthetic packed adapter per rank class (the content of a
+    # synthetic adapter does not change the bytes moved); N(0, 0.02) bf16
+    by_rank = {}
+    for r in sorted({c.rank for c in catalog.values()}):
+        by_rank[r] = (torch.randn(pages_for_rank(r) * page_bytes // 2) * 0.02).to(torch.bfloat16).view(
+            torch.uint8).pin_memory()
+    store = {a: by_rank[catalog[a].rank] for a in ids}
+    s = torch.cuda.Stream(device=dev)
+    cache = PagedAdapterCache(CacheConfig(), catalog, pool, host_store=store, compute_stream=s)
+    cache.set_capacity(n_pages * PagedAdapterCache.TOKENS_PER_PAGE, set(), 0)
+    groups = [[0, 1, 2], [3]]
+    ex = LoraStepExecutor(pool, max_requests=1024, max_tokens=4096, proj_groups=groups)
+    xs = [[torch.randn(T_DECODE, H, device=dev).to(torch.bfloat16) for _ in groups] for _ in range(N_LAYERS)]
+    ys = [[torch.randn(T_DECODE, H, device=dev).to(torch.bfloat16) for _ in range(N_PROJ)] for _ in range(N_LAYERS)]
+    p = np.asarray(probs)
+    slot_of = cache.slot_of
+    ones = np.ones(T_DECODE, dtype=np.int32)
+    state = {"now": 0, "graph": None}
+
+    def step(i):
+        rng = np.random.default_rng(rank * 1_000_003 + i)
+        batch = [ids[int(k)] for k in rng.choice(len(ids), T_DECODE, p=p)]
+        state["now"] += 20_000  # 20 ms per decode step, reference time units (us)
+        now = state["now"]
+        hints = set(batch)
+        waiters = {}
+        admitted = []
+        for a in batch:
+            e = cache.entries[a]
+            if e.resident:
+                cache.acquire(a, now)
+                admitted.append(a)
+                continue
+            cache.acquire(a, now)  # miss (counted)
+            if not e.loading:
+                try:
+                    cache.evict_until(e.spec.size_tokens, hints, now)
+                except InsufficientEvictableMemory:
+                    admitted.append(None)  # deferred (engine.py:526): the row runs without an adapter
+                    continue
+                cache.begin_load(a, now)
+            waiters.setdefault(a, []).append(a)
+            admitted.append(a)
+        batch = admitted
+        for a, w in waiters.items():
+            ev = cache.fill_event(a)
+            if ev is not None:
+                s.wait_event(ev)  # the apply reads the pages after the fill completed
+            cache.finish_load(a, now)
+            for _ in w:
+                cache.take_ref(a, now)
+        req_slot = np.array([slot_of(a) if a else -1 for a in batch], dtype=np.int32)
+        req_rank = np.array([catalog[a].rank if a else 0 for a in batch], dtype=np.int32)
+        with torch.cuda.stream(s):
+            ex.upload(req_slot, req_rank, ones, stream=s)
+            if state["graph"] is None:
+                ex.run(xs, ys)
+                g = torch.cuda.CUDAGraph()
+                s.synchronize()
+                with torch.cuda.graph(g, stream=s):
+                    ex.run(xs, ys)
+                state["graph"] = g
+            state["graph"].replay()
+        for a in batch:
+            if a:
+                cache.release(a, now)
+        state["deferred"] = state.get("deferred", 0) + sum(1 for a in batch if a is None)
+
+    for i in range(args.warmup * 4):  # warm the cache towards its steady state
+        step(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    h0, m0, l0, ev0, fb0 = cache.hits, cache.misses, cache.loads, cache.evictions, cache.fill_bytes
+    t0 = time.perf_counter()
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            step(args.warmup * 4 + i)
+        torch.cuda.synchronize(dev)
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    hits, misses = cache.hits - h0, cache.misses - m0
+    fill_b = cache.fill_bytes - fb0
+    # PCIe fill bandwidth alone: the largest adapter copied 5 times on the side stream
+    big = by_rank[max(by_rank)]
+    scratch = torch.empty(big.numel(), dtype=torch.uint8, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cache.fill_stream):
+        e0.record()
+        for _ in range(5):
+            scratch.copy_(big, non_blocking=True)
+        e1.record()
+    torch.cuda.synchronize(dev)
+    fill_gbs = 5 * big.numel() / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    if rank == 0:
+        tokens = T_DECODE * args.steps * world
+        line = {
+            "metric": METRIC, "value": tokens / el, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup * 4, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (one pinned random adapter image per rank class)",
+            "config": {"workload": "C4: 1000 adapters Zipf(0.7), PagedAdapterCache at 10% of idle HBM "
+                                   f"({n_pages} pages = {n_pages * page_bytes / 1e9:.1f} GB), decode batches of 256, "
+                                   "misses filled over PCIe on a side stream",
+                       "global_batch": T_DECODE * world, "seq_len": 1, "parallelism": f"replicas x{world}",
+                       "timing": "wall clock incl. host cache decisions and fills"},
+            "cache": {"hit_rate": hits / max(1, hits + misses), "hits": hits, "misses": misses,
+                      "loads": cache.loads - l0, "evictions": cache.evictions - ev0,
+                      "fill_bytes_per_step": fill_b / args.steps, "fill_gbs_during_run": fill_b / el / 1e9,
+                      "pcie_fill_gbs_alone": fill_gbs, "deferred_requests": state.get("deferred", 0)},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    pool.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -363,7 +508,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["qkv", "per-proj"], default="qkv")
-    ap.add_argument("--config", choices=["c2", "c3"], default="c2",
+    ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c2",
                     help="c2 (default, the BASELINE metric's decode config) or c3 (prefill, tcgen05 path)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -380,6 +525,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.config == "c4":
+            run_c4(args, rank, world)
         else:
             run_ours(args, rank, world)
     finally:

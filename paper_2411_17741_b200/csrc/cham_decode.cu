@@ -32,9 +32,9 @@
 
 namespace cham {
 int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
-                   void* const* ys, const int* perm, const int* seg_off, const int* seg_slot, const int* seg_rank,
-                   int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out, const float* v_in,
-                   int v_stride);
+                   void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
+                   const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out,
+                   const float* v_in, int v_stride);
 namespace decode {
 
 #ifndef CHAM_EXP_NOCOMPUTE
@@ -1131,8 +1131,8 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
     if (rc) return rc;
   }
   if (pre)
-    rc = prefill_launch(pool, layer, n_jobs, projs, xs, ys, perm, seg_off, seg_slot, seg_rank, n_seg, n_seg_dev,
-                        stream, mode, v_out, v_in, v_stride);
+    rc = prefill_launch(pool, layer, n_jobs, projs, xs, ys, n_tokens, perm, seg_off, seg_slot, seg_rank, n_seg,
+                        n_seg_dev, stream, mode, v_out, v_in, v_stride);
   return rc;
 }
 

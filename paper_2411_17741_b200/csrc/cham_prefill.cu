@@ -7,43 +7,48 @@
 //
 // Two launches per lora_apply (K3):
 //  P1 shrink  unit = (job, 128-token tile, K-split):  D1[128 x rp] (TMEM, fp32) =
-//             X_tile[128 x K/ks] . A^T[rp x K/ks]^T.  X rows are gathered through perm with
-//             cp.async (16-byte chunks written at their 128-byte-swizzled position), A^T
-//             pages are moved by 2 KiB TMA bulk copies straight from the page layout, which
-//             already is the K-major SWIZZLE_128B canonical layout.  The epilogue writes the
-//             fp32 partial v rows to a workspace (or, for the TP half, to v_out).
+//             X_tile[128 x K/ks] . A^T[rp x K/ks]^T.  X arrives by TMA tensor loads (one
+//             128-row box per 64-column stage when the tile's token rows are contiguous — the
+//             rows of a prefill request are — else one 1-row box per token: a TMA gather),
+//             A^T pages by 1 KiB bulk copies straight from the page layout, which already is
+//             the K-major SWIZZLE_128B canonical layout.  The epilogue writes fp32 partial
+//             v rows to a workspace (or, for the TP half, the final v to v_out).
 //  P2 expand  unit = (job, tile, 512 output columns):  V = sum of the K-split partials,
 //             rounded to bf16 into a K-major SWIZZLE_128B smem tile (zero beyond the rank);
-//             D2[128 x 128] (TMEM) = V . B where B pages are TMA-copied as MN-major
-//             SWIZZLE_128B operands (again the page layout itself); the epilogue adds D2
-//             to the gathered y rows (read-modify-write) — no separate elementwise kernel.
-// Both kernels are persistent (one CTA per SM), warp-specialised: epilogue warps 0-3
-// (TMEM lanes 0-127), loader warps, one MMA-issuing warp; smem rings are mbarrier pipelines
-// and TMEM accumulators are double-buffered so the epilogue of unit n overlaps the MMAs of
-// unit n+1.  The path is HBM-bound (AI ~15 flop/B at C3); tensor cores are used because the
-// CUDA-core FMA ceiling (~51-74 TFLOP/s) is below what the HBM roofline demands.
+//             per 64-column group D2[128 x 64] (TMEM) = V . B with the B page slices used as
+//             MN-major SWIZZLE_128B operands (again the page layout itself); the y tile of the
+//             group is TMA-loaded into the same stage, and the epilogue adds D2 and stores the
+//             rows back — no separate elementwise kernel.
+// Both kernels are persistent (one CTA per SM) and warp-specialised: warps 0-3 epilogue
+// (TMEM lanes 0-127, one token row per thread), warp 4 loads (TMA), warp 5 issues the MMAs.
+// Stage rings are mbarrier pipelines; TMEM accumulators are double-buffered so the epilogue
+// of one unit overlaps the MMAs of the next.  The path is HBM-bound (AI ~15 flop/B at C3);
+// tensor cores are used because the CUDA-core FMA ceiling (~51-74 TFLOP/s) is below what the
+// HBM roofline demands.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "cham_pool.h"
 
 namespace cham {
 namespace prefill {
 
 constexpr int BM = 128;                 // tokens per tile (UMMA M)
-constexpr int BK = 128;                 // shrink K elements per stage (two 64-element atoms)
+constexpr int BK = 64;                  // shrink K elements per stage (one 128-byte swizzle atom)
 constexpr int MAXR = kPrefillMaxRank;   // rank rows per adapter on this path
-constexpr int S1 = 3;                   // shrink ring stages
-constexpr int X_STAGE = BM * BK * 2;    // 32 KiB
-constexpr int A_STAGE = MAXR * BK * 2;  // 32 KiB
-constexpr int BN = 128;                 // expand N per MMA group (two atoms)
-constexpr int NSUB = 4;                 // expand groups per unit (512 columns)
+constexpr int S1 = 6;                   // shrink ring stages
+constexpr int X_STAGE = BM * 128;       // 16 KiB
+constexpr int A_STAGE = MAXR * 128;     // 16 KiB (one 1 KiB atom per page)
+constexpr int BN = 64;                  // expand N per MMA group (one atom)
+constexpr int NSUB = 8;                 // expand groups per unit (512 columns)
 constexpr int S2 = 4;                   // expand ring stages
-constexpr int B_STAGE = MAXR * BN * 2;  // 32 KiB (16 pages x 2 KiB)
+constexpr int B_STAGE = MAXR * 128;     // 16 KiB
+constexpr int Y_STAGE = BM * 128;       // 16 KiB
 constexpr int V_TILE = BM * MAXR * 2;   // 32 KiB
-constexpr int PAGE_SLICE = 2048;        // one page's share of a stage: 8 rows x 2 atoms
-constexpr int TMEM_COLS = 256;          // two 128-column fp32 accumulators
 constexpr int NSEG = kMaxSegments;
-
-constexpr int P1_THREADS = 320;  // warps 0-3 epilogue, 4-7 X loaders, 8 A loader, 9 MMA
-constexpr int P2_THREADS = 320;  // warps 0-7 V build + epilogue, 8 B loader, 9 MMA
+constexpr int NTHREADS = 192;           // warps 0-3 epilogue, 4 loader, 5 MMA
+constexpr int P1_TMEM = 256;            // two 128-column fp32 accumulators
+constexpr int P2_TMEM = 128;            // two 64-column fp32 accumulators
 
 struct Job {
   const char* x;
@@ -52,7 +57,15 @@ struct Job {
   long long b_off;
 };
 
-struct Params {
+// Activation tensor maps of one job (x for P1, y for P2): a 64-column x 128-row box for
+// contiguous tiles and a 64-column x 1-row box for gathered ones, both SWIZZLE_128B.
+struct alignas(64) Maps {
+  CUtensorMap tile;
+  CUtensorMap row;
+};
+
+struct alignas(64) Params {
+  Maps maps[kMaxJobs];
   const char* base;
   long long page_bytes;
   const int* slot_pages;
@@ -98,13 +111,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
-               "n"(TMEM_COLS));
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "n"(COLS));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
 }
+template <int COLS>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(TMEM_COLS));
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(COLS));
 }
 // 32 lanes x 32 consecutive fp32 columns: thread `lane` of the warp gets row (lane base + lane)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -122,13 +136,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+// 2-D TMA tensor load (box defined by the map) completing on an mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -208,7 +226,9 @@ __device__ __forceinline__ int choose_ks(const Params& p, int n_tiles) {
   const int nkc = p.h_in / BK;
   if (!p.split_ok) return 1;
   int ks = 1;
-  while (ks < kPrefillMaxSplit && n_tiles * p.n_jobs * ks < p.grid1 && nkc % (2 * ks) == 0) ks *= 2;
+  // about four units per CTA: balances the tail without shrinking the K loops below 8 stages
+  while (ks < kPrefillMaxSplit && n_tiles * p.n_jobs * ks < 4 * p.grid1 && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8)
+    ks *= 2;
   return ks;
 }
 
@@ -230,6 +250,43 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
   return u;
 }
 
+// Token rows of a unit's tile as seen by the loader warp: lane l holds rows l, l+32, l+64,
+// l+96 (perm applied); `contig` = the m rows are consecutive (one TMA box per stage).
+struct TileRows {
+  int row[4];
+  int first;
+  bool contig;
+};
+__device__ __forceinline__ TileRows tile_rows(const Params& p, int row0, int m, int lane) {
+  TileRows t;
+  bool ok = true;
+  t.first = p.perm ? __ldg(p.perm + row0) : row0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = lane + 32 * i;
+    const int pos = row0 + min(r, m - 1);
+    t.row[i] = p.perm ? __ldg(p.perm + pos) : pos;
+    if (r < m) ok &= t.row[i] == t.first + r;
+  }
+  t.contig = __all_sync(0xffffffffu, ok);
+  return t;
+}
+
+// Loader-warp helper: one activation stage (64 columns at c0) of the tile into smem.
+__device__ __forceinline__ void load_act(const Maps& mp, const TileRows& tr, int m, int c0, unsigned char* dst,
+                                         uint64_t* bar, uint64_t pol, int lane) {
+  if (tr.contig) {
+    if (lane == 0) tma_load_2d(dst, &mp.tile, c0, tr.first, bar, pol);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = lane + 32 * i;
+      if (r < m) tma_load_2d(dst + r * 128, &mp.row, c0, tr.row[i], bar, pol);
+    }
+  }
+}
+__device__ __forceinline__ uint32_t act_bytes(const TileRows& tr, int m) { return tr.contig ? BM * 128 : m * 128; }
+
 // =========================================================================== P1: shrink
 struct P1Shared {
   alignas(1024) unsigned char x[S1][X_STAGE];
@@ -239,13 +296,13 @@ struct P1Shared {
   TileList tl;
 };
 
-__global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(NTHREADS, 1) shrink_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   P1Shared& sm = *reinterpret_cast<P1Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < S1; ++i) {
-      mbar_init(&sm.full[i], 128 + 1);  // 128 X-loader threads + the A loader's expect_tx arrive
+      mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -254,8 +311,12 @@ __global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_cons
     }
     fence_mbar_init();
   }
-  if (warp == 9) {
-    tmem_alloc(&sm.tmem_base);
+  if (warp == 4 && lane < p.n_jobs) {
+    prefetch_map(&p.maps[lane].tile);
+    prefetch_map(&p.maps[lane].row);
+  }
+  if (warp == 5) {
+    tmem_alloc<P1_TMEM>(&sm.tmem_base);
     tc_fence_before();
   }
   build_tiles(p, sm.tl);  // contains __syncthreads
@@ -266,75 +327,36 @@ __global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_cons
   const int nkc = p.h_in / BK / ks;  // stages per unit
   const int n_units = n_tiles * ks * p.n_jobs;
 
-  if (warp >= 4 && warp < 8) {
-    // ---------------- X loaders: 128 threads, cp.async with a lag of S1-1 stages
-    const int t = tid - 128;
+  if (warp == 4) {
+    // ---------------- loader: X by TMA tensor loads, A^T by 1 KiB page bulk copies
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();  // the other jobs of the tile re-read x from L2
     int seq = 0;
     for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x) {
-      const int job = uu / (n_tiles * ks), rem = uu % (n_tiles * ks);
+      const int job = uu % p.n_jobs, rem = uu / p.n_jobs;
       const Unit u = make_unit(p, sm.tl, job, rem / ks);
       const int kq = rem % ks;
-      const char* xb = p.jobs[job].x;
-      // rows this thread copies: r = i*8 + t/16 (i = 0..15), chunk t%16 of the 256-byte stage row
-      const char* src_row[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int r = i * 8 + (t >> 4);
-        const int pos = u.row0 + min(r, u.m - 1);
-        const int row = p.perm ? __ldg(p.perm + pos) : pos;
-        src_row[i] = r < u.m ? xb + (long long)row * p.h_in * 2 : nullptr;
-      }
-      const int cc = t & 15, atom = cc >> 3, ch = cc & 7;
+      const TileRows tr = tile_rows(p, u.row0, u.m, lane);
+      const char* blk0 = p.base + p.jobs[job].a_off;
+      const long long pg = lane < u.np ? (long long)__ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + lane) : 0;
+      const uint32_t bytes = act_bytes(tr, u.m) + u.np * kAtomBytes;
       for (int k = 0; k < nkc; ++k, ++seq) {
         const int st = seq % S1;
         if (seq >= S1) mbar_wait(&sm.empty[st], ((seq / S1) - 1) & 1);
-        const int kel = (kq * nkc + k) * BK + atom * 64 + ch * 8;
-        const uint32_t dst0 = smem_u32(sm.x[st]) + atom * (BM * 128);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int r = i * 8 + (t >> 4);
-          if (src_row[i]) cp_async16(dst0 + swz(r, ch), src_row[i] + kel * 2);
-        }
-        cp_async_commit();
-        if (seq >= S1 - 1) {
-          cp_async_wait<S1 - 1>();
-          fence_proxy_async_shared();
-          mbar_arrive(&sm.full[(seq - (S1 - 1)) % S1]);
-        }
+        if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
+        __syncwarp();
+        const int kc = kq * nkc + k;
+        load_act(p.maps[job], tr, u.m, kc * BK, sm.x[st], &sm.full[st], pol_x, lane);
+        if (lane < u.np)
+          bulk_g2s(sm.a[st] + lane * kAtomBytes, blk0 + pg * p.page_bytes + (long long)kc * kAtomBytes, kAtomBytes,
+                   &sm.full[st], pol_w);
       }
     }
-    // drain: the last S1-1 stages
-    cp_async_wait<0>();
-    fence_proxy_async_shared();
-    for (int s = max(0, seq - (S1 - 1)); s < seq; ++s) mbar_arrive(&sm.full[s % S1]);
-  } else if (warp == 8) {
-    // ---------------- A^T loader: 2 KiB bulk copies per page per stage
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int seq = 0;
-      for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x) {
-        const int job = uu / (n_tiles * ks), rem = uu % (n_tiles * ks);
-        const Unit u = make_unit(p, sm.tl, job, rem / ks);
-        const int kq = rem % ks;
-        const char* blk0 = p.base + p.jobs[job].a_off;
-        for (int k = 0; k < nkc; ++k, ++seq) {
-          const int st = seq % S1;
-          if (seq >= S1) mbar_wait(&sm.empty[st], ((seq / S1) - 1) & 1);
-          mbar_arrive_expect_tx(&sm.full[st], u.np * PAGE_SLICE);
-          const long long koff = (long long)((kq * nkc + k) * BK / 64) * kAtomBytes;
-          for (int g = 0; g < u.np; ++g) {
-            const int page = __ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + g);
-            bulk_g2s(sm.a[st] + g * PAGE_SLICE, blk0 + (long long)page * p.page_bytes + koff, PAGE_SLICE,
-                     &sm.full[st], pol);
-          }
-        }
-      }
-    }
-  } else if (warp == 9) {
+  } else if (warp == 5) {
     // ---------------- MMA issuer
     int seq = 0, ui = 0;
     for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
-      const int job = uu / (n_tiles * ks), rem = uu % (n_tiles * ks);
+      const int job = uu % p.n_jobs, rem = uu / p.n_jobs;
       const Unit u = make_unit(p, sm.tl, job, rem / ks);
       const int acc = ui & 1;
       if (ui >= 2) mbar_wait(&sm.tempty[acc], ((ui >> 1) - 1) & 1);
@@ -349,8 +371,8 @@ __global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_cons
           const uint32_t xa = smem_u32(sm.x[st]), aa = smem_u32(sm.a[st]);
 #pragma unroll
           for (int j = 0; j < BK / 16; ++j) {
-            const uint64_t ad = sdesc(xa + (j >> 2) * (BM * 128) + (j & 3) * 32, 16, 1024);
-            const uint64_t bd = sdesc(aa + (j >> 2) * kAtomBytes + (j & 3) * 32, 16, PAGE_SLICE);
+            const uint64_t ad = sdesc(xa + j * 32, 16, 1024);
+            const uint64_t bd = sdesc(aa + j * 32, 16, kAtomBytes);
             mma_bf16(d, ad, bd, idesc, (k | j) ? 1u : 0u);
           }
           mma_commit(&sm.empty[st]);
@@ -363,7 +385,7 @@ __global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_cons
     // ---------------- epilogue warps 0-3: TMEM -> fp32 partial v rows
     int ui = 0;
     for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
-      const int job = uu / (n_tiles * ks), rem = uu % (n_tiles * ks);
+      const int job = uu % p.n_jobs, rem = uu / p.n_jobs;
       const Unit u = make_unit(p, sm.tl, job, rem / ks);
       const int kq = rem % ks;
       const int acc = ui & 1;
@@ -385,9 +407,9 @@ __global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_cons
     }
   }
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(tmem);
+    tmem_dealloc<P1_TMEM>(tmem);
   }
 }
 
@@ -395,30 +417,35 @@ __global__ void __launch_bounds__(P1_THREADS, 1) shrink_kernel(const __grid_cons
 struct P2Shared {
   alignas(1024) unsigned char v[2][V_TILE];
   alignas(1024) unsigned char b[S2][B_STAGE];
-  uint64_t bfull[S2], bempty[S2], vfull[2], vempty[2], tfull[2], tempty[2];
+  alignas(1024) unsigned char y[S2][Y_STAGE];
+  uint64_t full[S2], empty[S2], vfull[2], vempty[2], tfull[2], tempty[2];
   uint32_t tmem_base;
   TileList tl;
 };
 
-__global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(NTHREADS, 1) expand_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   P2Shared& sm = *reinterpret_cast<P2Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < S2; ++i) {
-      mbar_init(&sm.bfull[i], 1);
-      mbar_init(&sm.bempty[i], 1);
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1 + 128);  // MMA commit (B read) + 128 epilogue threads (y read)
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.vfull[i], 256);
+      mbar_init(&sm.vfull[i], 128);
       mbar_init(&sm.vempty[i], 1);
       mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 256);
+      mbar_init(&sm.tempty[i], 128);
     }
     fence_mbar_init();
   }
-  if (warp == 9) {
-    tmem_alloc(&sm.tmem_base);
+  if (warp == 4 && lane < p.n_jobs) {
+    prefetch_map(&p.maps[lane].tile);
+    prefetch_map(&p.maps[lane].row);
+  }
+  if (warp == 5) {
+    tmem_alloc<P2_TMEM>(&sm.tmem_base);
     tc_fence_before();
   }
   build_tiles(p, sm.tl);
@@ -430,39 +457,44 @@ __global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_cons
   const int nq = (p.h_out + ncols_unit - 1) / ncols_unit;
   const int n_units = n_tiles * nq * p.n_jobs;
 
-  if (warp == 8) {
-    // ---------------- B loader: per 128-column group, one 2 KiB bulk copy per page
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int seq = 0;
-      for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x) {
-        const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
-        const Unit u = make_unit(p, sm.tl, job, rem / nq);
-        const int n0 = (rem % nq) * ncols_unit;
-        const int nsub = min(NSUB, (p.h_out - n0) / BN);
-        const char* blk0 = p.base + p.jobs[job].b_off;
-        for (int c = 0; c < nsub; ++c, ++seq) {
-          const int st = seq % S2;
-          if (seq >= S2) mbar_wait(&sm.bempty[st], ((seq / S2) - 1) & 1);
-          if (u.rp / kRowsPerPage > u.np) {
-            // odd page count: the pad page (K rows rank..rp) must be finite — zero it
-            uint4* z = reinterpret_cast<uint4*>(sm.b[st] + u.np * PAGE_SLICE);
-            for (int i = 0; i < PAGE_SLICE / 16; ++i) z[i] = make_uint4(0, 0, 0, 0);
-            fence_proxy_async_shared();
-          }
-          mbar_arrive_expect_tx(&sm.bfull[st], u.np * PAGE_SLICE);
-          const long long noff = (long long)((n0 + c * BN) / 64) * kAtomBytes;
-          for (int g = 0; g < u.np; ++g) {
-            const int page = __ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + g);
-            bulk_g2s(sm.b[st] + g * PAGE_SLICE, blk0 + (long long)page * p.page_bytes + noff, PAGE_SLICE,
-                     &sm.bfull[st], pol);
-          }
+  if (warp == 4) {
+    // ---------------- loader: per 64-column group, one 1 KiB B slice per page + the y tile
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_y = policy_evict_last();  // written back right after
+    int seq = 0;
+    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x) {
+      const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
+      const Unit u = make_unit(p, sm.tl, job, rem / nq);
+      const int n0 = (rem % nq) * ncols_unit;
+      const int nsub = min(NSUB, (p.h_out - n0) / BN);
+      const TileRows tr = tile_rows(p, u.row0, u.m, lane);
+      const char* blk0 = p.base + p.jobs[job].b_off;
+      const long long pg = lane < u.np ? (long long)__ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + lane) : 0;
+      const bool pad = u.rp / kRowsPerPage > u.np;  // odd page count: zero pad page (K rows rank..rp)
+      const uint32_t bytes = act_bytes(tr, u.m) + u.np * kAtomBytes;
+      for (int c = 0; c < nsub; ++c, ++seq) {
+        const int st = seq % S2;
+        if (seq >= S2) mbar_wait(&sm.empty[st], ((seq / S2) - 1) & 1);
+        if (pad) {
+          uint4* z = reinterpret_cast<uint4*>(sm.b[st] + u.np * kAtomBytes);
+          z[lane] = make_uint4(0, 0, 0, 0);
+          z[lane + 32] = make_uint4(0, 0, 0, 0);
+          fence_proxy_async_shared();
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
+        __syncwarp();
+        const int col = n0 + c * BN;
+        if (lane < u.np)
+          bulk_g2s(sm.b[st] + lane * kAtomBytes, blk0 + pg * p.page_bytes + (long long)(col / 64) * kAtomBytes,
+                   kAtomBytes, &sm.full[st], pol_w);
+        load_act(p.maps[job], tr, u.m, col, sm.y[st], &sm.full[st], pol_y, lane);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 5) {
     // ---------------- MMA issuer
     int seq = 0, gi = 0, ui = 0;
+    const uint32_t idesc = idesc_bf16(BM, BN, true);
     for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
       const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
       const Unit u = make_unit(p, sm.tl, job, rem / nq);
@@ -471,20 +503,19 @@ __global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_cons
       const int vb = ui & 1;
       mbar_wait(&sm.vfull[vb], (ui >> 1) & 1);
       tc_fence_after();
-      const uint32_t idesc = idesc_bf16(BM, BN, true);
       for (int c = 0; c < nsub; ++c, ++seq, ++gi) {
         const int st = seq % S2, acc = gi & 1;
         if (gi >= 2) mbar_wait(&sm.tempty[acc], ((gi >> 1) - 1) & 1);
-        mbar_wait(&sm.bfull[st], (seq / S2) & 1);
+        mbar_wait(&sm.full[st], (seq / S2) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t va = smem_u32(sm.v[vb]), ba = smem_u32(sm.b[st]);
           for (int j = 0; j < u.rp / 16; ++j) {
             const uint64_t ad = sdesc(va + (j >> 2) * (BM * 128) + (j & 3) * 32, 16, 1024);
-            const uint64_t bd = sdesc(ba + j * 2 * PAGE_SLICE, kAtomBytes, PAGE_SLICE);
+            const uint64_t bd = sdesc(ba + j * 2 * kAtomBytes, kAtomBytes, kAtomBytes);
             mma_bf16(tmem + acc * BN, ad, bd, idesc, j ? 1u : 0u);
           }
-          mma_commit(&sm.bempty[st]);
+          mma_commit(&sm.empty[st]);
           mma_commit(&sm.tfull[acc]);
           if (c == nsub - 1) mma_commit(&sm.vempty[vb]);
         }
@@ -492,10 +523,9 @@ __global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_cons
       }
     }
   } else {
-    // ---------------- warps 0-7: build V (bf16, swizzled) then the y epilogue
-    const int q = warp & 3, half = warp >> 2;
-    const int r = q * 32 + lane;  // tile row == TMEM lane
-    int gi = 0, ui = 0;
+    // ---------------- warps 0-3: build V (bf16, swizzled), then y += D2 per group
+    const int r = warp * 32 + lane;  // tile row == TMEM lane
+    int seq = 0, gi = 0, ui = 0;
     for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
       const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
       const Unit u = make_unit(p, sm.tl, job, rem / nq);
@@ -505,13 +535,11 @@ __global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_cons
       const bool valid = r < u.m;
       const int pos = u.row0 + min(r, u.m - 1);
       const int row = p.perm ? __ldg(p.perm + pos) : pos;
-      // V rows: this thread fills 8-column chunks [half * rp/2, (half+1) * rp/2) of row r
       if (ui >= 2) mbar_wait(&sm.vempty[vb], ((ui >> 1) - 1) & 1);
       {
         const float* vsrc = p.vin + job * p.v_job_stride + (long long)pos * p.ld;
         const uint32_t vbase = smem_u32(sm.v[vb]);
-        const int c_lo = half * (u.rp / 16), c_hi = c_lo + u.rp / 16;  // 8-col chunk indices
-        for (int cj = c_lo; cj < c_hi; ++cj) {
+        for (int cj = 0; cj < u.rp / 8; ++cj) {
           float f[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) f[i] = 0.f;
@@ -533,24 +561,23 @@ __global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_cons
       }
       fence_proxy_async_shared();
       mbar_arrive(&sm.vfull[vb]);
-      // epilogue per 128-column group: y[row, n0 + c*128 + half*64 .. +64] += D2
       char* yrow = p.jobs[job].y + (long long)row * p.h_out * 2;
-      for (int c = 0; c < nsub; ++c, ++gi) {
-        const int acc = gi & 1;
-        const int col0 = n0 + c * BN + half * 64;
-        uint4 yv[8];
-        if (valid) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) yv[i] = *reinterpret_cast<const uint4*>(yrow + (col0 + i * 8) * 2);
-        }
+      for (int c = 0; c < nsub; ++c, ++seq, ++gi) {
+        const int st = seq % S2, acc = gi & 1;
+        const int col0 = n0 + c * BN;
         mbar_wait(&sm.tfull[acc], (gi >> 1) & 1);
         tc_fence_after();
         float d0[32], d1[32];
-        const uint32_t ta = tmem + acc * BN + half * 64 + ((uint32_t)(q * 32) << 16);
+        const uint32_t ta = tmem + acc * BN + ((uint32_t)(warp * 32) << 16);
         tmem_ld32(ta, d0);
         tmem_ld32(ta + 32, d1);
         tc_fence_before();
         mbar_arrive(&sm.tempty[acc]);
+        mbar_wait(&sm.full[st], (seq / S2) & 1);  // the y tile of this group has landed
+        uint4 yv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) yv[i] = lds128(sm.y[st] + swz(r, i));
+        mbar_arrive(&sm.empty[st]);
         if (valid) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -566,20 +593,49 @@ __global__ void __launch_bounds__(P2_THREADS, 1) expand_kernel(const __grid_cons
     }
   }
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(tmem);
+    tmem_dealloc<P2_TMEM>(tmem);
   }
 }
 
 }  // namespace prefill
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// [rows x cols] bf16 row-major activation: boxes of 64 columns x box_rows rows, 128-byte swizzle
+int encode_act_map(CUtensorMap* m, const void* base, int rows, int cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CHAM_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHAM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CHAM_OK;
+}
+}  // namespace
+
 // Launch P1 (unless mode == expand-only) and P2 (unless mode == shrink-only) for the
 // prefill segments of this apply.  mode: 0 fused, 1 shrink (v_out), 2 expand (v_in).
 int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
-                   void* const* ys, const int* perm, const int* seg_off, const int* seg_slot, const int* seg_rank,
-                   int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out, const float* v_in,
-                   int v_stride) {
+                   void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
+                   const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out,
+                   const float* v_in, int v_stride) {
   using namespace prefill;
   static bool attr_set = false;
   if (!attr_set) {
@@ -626,11 +682,21 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
     prm.vin = v_in;
   }
   if (mode != 2) {
-    shrink_kernel<<<pool->sm_count, P1_THREADS, sizeof(P1Shared), s>>>(prm);
+    for (int j = 0; j < n_jobs; ++j) {
+      int rc = encode_act_map(&prm.maps[j].tile, xs[j], n_tokens, prm.h_in, BM);
+      if (!rc) rc = encode_act_map(&prm.maps[j].row, xs[j], n_tokens, prm.h_in, 1);
+      if (rc) return rc;
+    }
+    shrink_kernel<<<pool->sm_count, NTHREADS, sizeof(P1Shared), s>>>(prm);
     CHAM_CUDA(cudaGetLastError());
   }
   if (mode != 1) {
-    expand_kernel<<<pool->sm_count, P2_THREADS, sizeof(P2Shared), s>>>(prm);
+    for (int j = 0; j < n_jobs; ++j) {
+      int rc = encode_act_map(&prm.maps[j].tile, ys[j], n_tokens, prm.h_out, BM);
+      if (!rc) rc = encode_act_map(&prm.maps[j].row, ys[j], n_tokens, prm.h_out, 1);
+      if (rc) return rc;
+    }
+    expand_kernel<<<pool->sm_count, NTHREADS, sizeof(P2Shared), s>>>(prm);
     CHAM_CUDA(cudaGetLastError());
   }
   return CHAM_OK;

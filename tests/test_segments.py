@@ -124,3 +124,19 @@ def test_live_step_duration_lora_term(reference_pkg, sim_steps):
         with_lora = cm.step_duration(pre, dec, ranks)
         without = cm.step_duration(pre, dec, {a: 0 for a in ranks})
         assert abs((with_lora - without) - coef * st["adapter_units"]) <= 1.0
+
+
+def test_segment_token_bounds_route_hints():
+    """Host routing hints (executor.segment_token_bounds): one segment per distinct slot,
+    min/max of their token counts; a rank above the tcgen05 limit forces min = 0."""
+    from paper_2411_17741_b200.executor import segment_token_bounds
+    from oracle.segments_ref import build_segments_ref
+
+    slots = [3, 1, 3, -1, 7, 1]
+    ranks = [16, 8, 16, 0, 64, 8]
+    ntok = [100, 1, 40, 9, 70, 2]
+    perm, off, sl, rk = build_segments_ref(slots, ranks, ntok)
+    lens = [int(off[i + 1] - off[i]) for i in range(len(sl)) if sl[i] >= 0]
+    assert segment_token_bounds(slots, ranks, ntok) == (min(lens), max(lens)) == (3, 140)
+    assert segment_token_bounds(slots, [16, 8, 16, 0, 256, 8], ntok) == (0, 140)
+    assert segment_token_bounds([-1, -1], [0, 0], [5, 5]) == (0, 0)
