@@ -41,34 +41,48 @@ namespace decode {
 #define CHAM_EXP_NOCOMPUTE 0  // experiment builds only: consumers skip the math (data-movement ceiling)
 #endif
 constexpr bool kNoCompute = CHAM_EXP_NOCOMPUTE != 0;
+#ifndef CHAM_SHRINK_LPT
+#define CHAM_SHRINK_LPT 1  // shrink units in LPT order (else segment order)
+#endif
+constexpr bool kShrinkLpt = CHAM_SHRINK_LPT != 0;
 constexpr int TG = 4;                        // tokens per tile
 constexpr int NSTAGE = 4;
 constexpr int A_CHUNK = 32768;               // K1: adapter bytes per stage (8 rows x 4 KiB)
 constexpr int X_ROW = A_CHUNK / kRowsPerPage;  // K1: x bytes per token per stage (k-chunk)
 static_assert(X_ROW == kActRowBytes, "pool workspace geometry");
 constexpr int K1_STAGE = A_CHUNK + TG * X_ROW;
-// K2 geometry.  Tiles of adapters with >= 16 pages (rank >= 128) use 512-column units with
-// 4 pages per stage (8 KiB per page copy); smaller ranks use 1024-column units with 2 pages
-// per stage (16 KiB copies).  Either way a stage holds 32 KiB of B and no unit exceeds 4
-// stages for ranks <= 128, which keeps the dynamic dispatch balanced at the phase end.
-#ifndef CHAM_BIG_PAGES
-#define CHAM_BIG_PAGES 33  // > kMaxPagesPerSlot: disabled (A/B on C2: 102.7k vs 101.6k tok/s)
+// K2 geometry tiers, chosen by the adapter's page count np so that every expand unit is at
+// most two 32 KiB stages (uniform units keep the dynamic dispatch balanced to the end —
+// with unit sizes from 16 to 256 KiB, large units claimed late by the look-ahead dispatch
+// made an ~8 us tail):
+//   tier 0 (np <= 4):  units of 2048 B per B row, 2 pages per stage (16 KiB page copies)
+//   tier 1 (np <= 8):  1024 B per B row, 4 pages per stage (8 KiB copies)
+//   tier 2 (np <= 16): 512 B per B row, 8 pages per stage (4 KiB copies)
+constexpr int NTIER = 3;
+constexpr int NCB_SMALL = 2048;              // bytes of one B row per unit, tier 0
+__host__ __device__ constexpr int tier_ncb(int t) { return NCB_SMALL >> t; }
+__host__ __device__ constexpr int tier_pitch(int t) {  // page pitch in a stage (+ bank skew)
+  return (NCB_SMALL >> t) * kRowsPerPage + (64 >> t);
+}
+#ifndef CHAM_TIERS
+#define CHAM_TIERS 0  // 1: page-count tiers (A/B on C2: 98.1k vs 110.3k tok/s without)
 #endif
-constexpr int kBigPages = CHAM_BIG_PAGES;    // np >= kBigPages: "big" unit geometry
-constexpr int NCB_SMALL = 2048;              // bytes of one B row per unit (np < kBigPages)
-constexpr int NCB_BIG = 1024;                // bytes of one B row per unit (np >= kBigPages)
-constexpr int PITCH_SMALL = NCB_SMALL * kRowsPerPage + 64;  // page pitch in a stage (+bank skew)
-constexpr int PITCH_BIG = NCB_BIG * kRowsPerPage + 32;
-constexpr int K2_B = 2 * PITCH_SMALL;
-static_assert(4 * PITCH_BIG <= K2_B, "stage layout");
+__host__ __device__ constexpr int tier_of_np(int np) {
+  return CHAM_TIERS == 0 ? 0 : np <= 4 ? 0 : np <= 8 ? 1 : 2;
+}
+constexpr int K2_B = 2 * tier_pitch(0);
+static_assert(4 * tier_pitch(1) <= K2_B && 8 * tier_pitch(2) <= K2_B, "stage layout");
 constexpr int K2_Y = K2_B;
 constexpr int K2_V = K2_Y + TG * NCB_SMALL;
-constexpr int K2_STAGE = K2_V + 4 * TG * kRowsPerPage * 4;  // v slice [page][token][8 rows]
+constexpr int K2_STAGE = K2_V + 8 * TG * kRowsPerPage * 4;  // v slice [page][token][8 rows]
+constexpr int PQ = 16;             // publisher ring depth (tile counters to release)
 constexpr int GROUP_WARPS = 8;
 constexpr int GROUP_THREADS = GROUP_WARPS * 32;
-constexpr int NTHREADS = 32 + GROUP_THREADS;
-static_assert(GROUP_THREADS == 2 * (NCB_SMALL / 16) && GROUP_THREADS == 4 * (NCB_BIG / 16),
-              "K2 maps 2 (small) or 4 (big) threads per 16-byte column chunk");
+constexpr int NTHREADS = 32 + GROUP_THREADS;      // plan kernel; apply kernel adds the publisher warp
+constexpr int APPLY_THREADS = NTHREADS + 32;
+static_assert(GROUP_THREADS == 2 * (tier_ncb(0) / 16) && GROUP_THREADS == 4 * (tier_ncb(1) / 16) &&
+                  GROUP_THREADS == 8 * (tier_ncb(2) / 16),
+              "K2 maps 2 << tier threads per 16-byte column chunk");
 constexpr int PLAN_SEGS = 512;
 constexpr int PLAN_PAGES = 2048;
 constexpr int PLAN_TOKENS = 2048;
@@ -97,8 +111,8 @@ struct Params {
   const int* seg_rank;
   int n_seg;
   const int* n_seg_dev;
-  int* ctr;        // [0] next shrink unit, [1] finished CTAs, [4] next expand unit,
-                   // [8] grid-barrier arrivals, [9] grid-barrier generation
+  int* ctr;        // [0] next shrink unit, [1] finished CTAs, [4] next expand unit
+  int* tile_ctr;   // MODE_FUSED: [job][expand tile] shrink units finished (v rows published)
   int* err;
   float* vws;      // this apply's compact v buffer: [job][sum_s T_s * rpad_s]
   long long vws_job_stride;
@@ -136,7 +150,7 @@ struct alignas(16) Plan {
   int seg_sr[PLAN_SEGS];      // (slot << 9) | rank
   int seg_pg[PLAN_SEGS + 1];  // prefix of pages -> pages[]
   int v_start[PLAN_SEGS + 1]; // prefix of nt_s * TG * rpad_s -> v, per tile [page][TG][8]
-  int sh_start[PLAN_SEGS + 1];  // K1 units prefix (segment order)
+  int sh_start[PLAN_SEGS + 1];  // K1 units prefix (LPT order, indexed by segment)
   int ex_start[PLAN_SEGS + 1];  // K2 tiles prefix (LPT order); units = tiles x column chunks
   int order[PLAN_SEGS];         // K2 segment order: decreasing page count
   int bucket[kMaxPagesPerSlot + 2];
@@ -145,8 +159,8 @@ struct alignas(16) Plan {
   int scan[NTHREADS / 32][4];
   int totals[6];  // K1 units/job, K2 tiles/job, tokens, pages, v floats/job, segments with work
   int n_seg;
-  int n_big_tiles;           // leading LPT tiles whose adapters have >= kBigPages pages
-  int nb_seg;
+  int tier_tiles[NTIER];     // leading LPT tiles of tier >= t (tier_tiles[0] = all tiles)
+  int tier_seg[NTIER];       // leading LPT segments of tier >= t
   int order_pos[PLAN_SEGS];  // segment -> position in the LPT order
   long long desc_cap;        // descriptor capacity (entries) after the header
 };
@@ -177,7 +191,9 @@ struct Shared {
   uint64_t empty[NSTAGE];
   Meta meta[NSTAGE];
   uint64_t plan_bar;
-  int grid_gen;  // grid-barrier generation observed at kernel start
+  int last_cta;  // this CTA re-arms the counters at exit
+  int* pub_slot[PQ];
+  uint64_t pub_full[PQ], pub_empty[PQ];
   int unit_mailbox;
   Plan plan;
 };
@@ -238,8 +254,8 @@ __device__ __forceinline__ int n_kchunks(const Params& p) {
   return ceil_div(p.h_in * Elem<T>::kBytes, X_ROW);
 }
 template <typename T>
-__device__ __forceinline__ int n_colchunks(const Params& p, bool big) {
-  return ceil_div(p.h_out * Elem<T>::kBytes, big ? NCB_BIG : NCB_SMALL);
+__device__ __forceinline__ int n_colchunks(const Params& p, int tier) {
+  return ceil_div(p.h_out * Elem<T>::kBytes, tier_ncb(tier));
 }
 
 // Builds the launch plan in shared memory (all NTHREADS threads).  It depends only on the
@@ -258,7 +274,9 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
     // segments of the tcgen05 prefill path carry no decode work (rank 0 here)
     const bool pre = is_prefill_segment(o1 - o0, rank, p.prefill_thr);
     pl.seg_sr[s] = (slot >= 0 && !pre) ? ((slot << 9) | rank) : 0;
-    const int np = ceil_div(rank, kRowsPerPage);
+    // same page count as the second pass (0 for prefill-routed segments): the unit, page and
+    // v prefixes must not leave holes
+    const int np = (slot >= 0 && !pre) ? ceil_div(rank, kRowsPerPage) : 0;
     const int nt = ceil_div(o1 - o0, TG);
     lsh += nt * np;
     lpg += np;
@@ -307,13 +325,15 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
   // LPT order for K2: bucket offsets by decreasing page count, then scatter segments
   if (tid == 0) {
     int acc = 0;
-    pl.nb_seg = 0;
+    for (int t = 0; t < NTIER; ++t) pl.tier_seg[t] = 0;
     for (int np = kMaxPagesPerSlot; np >= 1; --np) {
       const int c = pl.bucket[np];
       pl.bucket[np] = acc;
       acc += c;
-      if (np >= kBigPages) pl.nb_seg = acc;  // segments with >= kBigPages pages lead the order
+      for (int t = 1; t < NTIER; ++t)
+        if (tier_of_np(np) >= t) pl.tier_seg[t] = acc;  // higher tiers lead the order
     }
+    pl.tier_seg[0] = acc;
     pl.totals[5] = acc;  // segments with work
   }
   __syncthreads();
@@ -339,30 +359,39 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
       pl.perm[i] = (uint16_t)(p.perm ? __ldg(p.perm + i) : i);
   }
   __syncthreads();
-  // K2 unit prefix over the LPT order (one warp scans; <= 512 entries)
+  // K2 tile prefix and K1 unit prefix over the LPT order (one warp scans; <= 512 entries).
+  // Both phases walk the segments largest-rank first: when the first expand units are
+  // dispatched, the shrink units still in flight belong to the small tiles at the end of the
+  // order, so the per-tile v-ready waits of the expand producer almost never block.
   const int nw = pl.totals[5];
   if (warp == 0) {
-    int carry = 0;
+    int carry = 0, carry_sh = 0;
     for (int base = 0; base < nw; base += 32) {
       const int i = base + lane;
-      int u = 0;
+      int u = 0, ush = 0, s = 0;
       if (i < nw) {
-        const int s = pl.order[i];
+        s = pl.order[i];
         u = ceil_div(pl.seg_off[s + 1] - pl.seg_off[s], TG);
+        ush = u * ceil_div(pl.seg_sr[s] & 511, kRowsPerPage);
       }
-      int inc = u;
+      int inc = u, inc_sh = ush;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int a = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += a;
+        const int b = __shfl_up_sync(0xffffffffu, inc_sh, o);
+        if (lane >= o) { inc += a; inc_sh += b; }
       }
-      if (i < nw) pl.ex_start[i] = carry + inc - u;
+      if (i < nw) {
+        pl.ex_start[i] = carry + inc - u;
+        if (kShrinkLpt) pl.sh_start[s] = carry_sh + inc_sh - ush;
+      }
       carry += __shfl_sync(0xffffffffu, inc, 31);
+      carry_sh += __shfl_sync(0xffffffffu, inc_sh, 31);
     }
     if (lane == 0) {
       pl.ex_start[nw] = carry;
       pl.totals[1] = carry;
-      pl.n_big_tiles = pl.ex_start[pl.nb_seg];
+      for (int t = 0; t < NTIER; ++t) pl.tier_tiles[t] = pl.ex_start[pl.tier_seg[t]];
     }
   }
   __syncthreads();
@@ -417,6 +446,10 @@ __device__ __forceinline__ bool prologue(const Params& p, Shared& sm) {
       mbar_init(&sm.empty[i], GROUP_THREADS);
     }
     mbar_init(&sm.plan_bar, 1);
+    for (int i = 0; i < PQ; ++i) {
+      mbar_init(&sm.pub_full[i], 1);
+      mbar_init(&sm.pub_empty[i], 1);
+    }
     fence_mbar_init();
     mbar_arrive_expect_tx(&sm.plan_bar, sizeof(Plan));
     bulk_g2s(&sm.plan, p.plan, sizeof(Plan), &sm.plan_bar, policy_evict_last());
@@ -448,9 +481,21 @@ __device__ __forceinline__ void trace_consumer(const Params& p, int seq, int fie
 // =========================================================================== K1: shrink
 // One unit: nst stages (k-chunks) of one page of one tile; the consumers keep the 8 x NT
 // dot products in registers across the stages and write the final v rows at the end.
+// The v rows of a finished shrink unit are released to the expand producers (tile counter
+// += 1) by a dedicated publisher warp: its gpu-scope fence waits for the stores to be
+// acknowledged, which would otherwise stall a consumer warp (and with it the stage release)
+// for a full store round trip on every unit.
+__device__ __forceinline__ void post_publish(Shared& sm, int& npub, int* ctr) {
+  const int k = npub++;
+  const int slot = k % PQ;
+  if (k >= PQ) mbar_wait(&sm.pub_empty[slot], ((k / PQ) - 1) & 1);
+  sm.pub_slot[slot] = ctr;
+  mbar_arrive(&sm.pub_full[slot]);
+}
+
 template <typename T, int NT>
 __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1Shared& sm, int& seq, const Meta& m0,
-                                            float* red, int ct, int lane, int gw) {
+                                            float* red, int ct, int lane, int gw, int& npub) {
   constexpr int ES = Elem<T>::kBytes;
   constexpr int EPV = Elem<T>::kEPV;
   constexpr int NP2 = EPV / 2;
@@ -511,7 +556,16 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
         const int tile = (m0.pos0 - pl.seg_off[m0.seg]) / TG;
         const long long vb = pl.v_start[m0.seg] + (long long)tile * TG * m0.np * kRowsPerPage;
         p.vws[m0.job * p.vws_job_stride + vb + (m0.g * TG + t) * kRowsPerPage + j] = sum;
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // read later by TMA (async proxy)
       }
+    }
+  }
+  if (p.tile_ctr && gw == 0) {
+    // this page's v rows of the tile are final: hand the tile counter to the publisher warp
+    __syncwarp();
+    if (lane == 0) {
+      const int tile = pl.ex_start[pl.order_pos[m0.seg]] + (m0.pos0 - pl.seg_off[m0.seg]) / TG;
+      post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile);
     }
   }
 }
@@ -543,7 +597,7 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
     const unsigned char* st = sm.stage[stage];
     const float* Vst = reinterpret_cast<const float*>(st + K2_V);  // [page in stage][TG][8]
     if (active && !kNoCompute) {
-      if (lpg == 2 || m.npg == 2) {
+      if (lpg >= 2 || m.npg == 2) {
         // own page pg0 + h: all 8 rows, fully unrolled
         if (h < m.npg) {
           const unsigned char* Bg = st + h * m0.pitch;
@@ -755,39 +809,76 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
   const int J = p.n_jobs;
-  const int ncc_b = n_colchunks<T>(p, true), ncc_s = n_colchunks<T>(p, false);
-  const int NB = pl.n_big_tiles, NTL = pl.totals[1];
-  const int units_big = NB * J * ncc_b;
-  const int total = units_big + (NTL - NB) * J * ncc_s;
+  const int NTL = pl.totals[1];
+  // unit space: tier 2 tiles, then tier 1, then tier 0 (the LPT order); inside a tier
+  // unit = (tile * n_jobs + job) * ncc + column chunk
+  int ubase[NTIER + 1], ncc[NTIER];
+  ubase[NTIER] = 0;
+#pragma unroll
+  for (int t = NTIER - 1; t >= 0; --t) {
+    ncc[t] = n_colchunks<T>(p, t);
+    const int t_end = t == 0 ? NTL : pl.tier_tiles[t];
+    const int t_beg = t == NTIER - 1 ? 0 : pl.tier_tiles[t + 1];
+    ubase[t] = ubase[t + 1] + (t_end - t_beg) * J * ncc[t];
+  }
+  const int total = ubase[0];
   const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
   const UnitDesc* desc =
       reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan)) + pl.totals[0];
   const uint64_t pol_w = policy_evict_first();
-  auto tile_of = [&](int u) { return u < units_big ? u / (J * ncc_b) : NB + (u - units_big) / (J * ncc_s); };
-  bool v_ready = !fused;
+  // unit -> (tier, tile, job * ncc + column chunk)
+  auto decode_unit = [&](int u, int& tier, int& jc) {
+    tier = u < ubase[2] ? 2 : u < ubase[1] ? 1 : 0;
+    const int rel = u - (tier == 2 ? 0 : ubase[tier + 1]);
+    const int tile0 = tier == 2 ? 0 : pl.tier_tiles[tier + 1];
+    jc = rel % (J * ncc[tier]);
+    return tile0 + rel / (J * ncc[tier]);
+  };
+  auto tile_of = [&](int u) {
+    int t, jc;
+    return decode_unit(u, t, jc);
+  };
   UnitQueue uq;
   uq.init(p.ctr + 4, total, 2, lane, &sm.unit_mailbox);
+  // tile-ready counter of a unit, loaded without blocking (relaxed) when the unit is claimed
+  auto peek_ready = [&](int u) {
+    int t, jc;
+    const int tl = decode_unit(u, t, jc);
+    int v = 0;
+    if (fused && lane == 0) {
+      const int* c = p.tile_ctr + (jc / ncc[t]) * NTL + tl;
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    }
+    return v;
+  };
   int unit = uq.next(lane);
   int4 da = make_int4(0, 0, 0, 0), db = da;
-  if (unit >= 0) ldg_desc(desc + tile_of(unit), da, db);
+  int rdy = 0;
+  if (unit >= 0) {
+    ldg_desc(desc + tile_of(unit), da, db);
+    rdy = peek_ready(unit);
+  }
   while (unit >= 0) {
     const int nunit = uq.next(lane);
     int4 na = da, nb = db;
-    if (nunit >= 0) ldg_desc(desc + tile_of(nunit), na, nb);
-    const bool big = unit < units_big;
-    const int ncc = big ? ncc_b : ncc_s;
-    const int jc = (big ? unit : unit - units_big) % (J * ncc);
-    const int job = jc / ncc;
-    const int cc = jc - job * ncc;
+    int nrdy = 0;
+    if (nunit >= 0) {
+      ldg_desc(desc + tile_of(nunit), na, nb);
+      nrdy = peek_ready(nunit);
+    }
+    int tier, jc;
+    const int tile = decode_unit(unit, tier, jc);
+    const int job = jc / ncc[tier];
+    const int cc = jc - job * ncc[tier];
     const int s = da.x, pos0 = da.y;
     const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff;
     const int vbase = da.w;
     const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
     const int slot = pl.seg_sr[s] >> 9;
-    const int lpg = big ? 2 : 1;
+    const int lpg = tier + 1;
     const int pgs = 1 << lpg;
-    const int ncb = big ? NCB_BIG : NCB_SMALL;
-    const int pitch = big ? PITCH_BIG : PITCH_SMALL;
+    const int ncb = tier_ncb(tier);
+    const int pitch = tier_pitch(tier);
     const int ncol_unit = ncb / ES;
     const int col0 = cc * ncol_unit;
     const int ncols = min(ncol_unit, p.h_out - col0);
@@ -845,14 +936,15 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
       if (k == nst - 1 && lane < tcount)
         bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage],
                  pol_w);
-      if (!v_ready) {
-        // v of every tile is complete once all CTAs passed the phase-1 barrier
-        if (lane == 0) {
-          while (ld_acquire_gpu(p.ctr + 9) == sm.grid_gen) __nanosleep(32);
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+      if (fused && k == 0) {
+        // the tile's v rows are complete once all np shrink units of (job, tile) published
+        // (writers: v stores, proxy fence, gpu fence, counter).  The counter was peeked when
+        // the unit was claimed; only a tile still in flight then is polled here.
+        if (lane == 0 && rdy < np) {
+          const int* c = p.tile_ctr + job * NTL + tile;
+          while (ld_acquire_gpu(c) < np) __nanosleep(20);
         }
         __syncwarp();
-        v_ready = true;
       }
       if (p.v_in) {
         // TP: v [position][v_stride] -> stage [page][token][8], one 32-byte copy each
@@ -878,11 +970,12 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
     unit = nunit;
     da = na;
     db = nb;
+    rdy = nrdy;
   }
   return seq;
 }
 
-// Marker stage between the phases: consumers arrive at the grid barrier on it.
+// Marker stage (end of the unit stream).
 __device__ __forceinline__ void post_marker(Shared& sm, int seq, int kind) {
   const int st = seq % NSTAGE;
   mbar_wait(&sm.empty[st], ((seq / NSTAGE) & 1) ^ 1);
@@ -890,27 +983,15 @@ __device__ __forceinline__ void post_marker(Shared& sm, int seq, int kind) {
   mbar_arrive(&sm.full[st]);
 }
 
-// Consumers of this CTA finished phase 1: publish (release) and count the CTA in.
-__device__ __forceinline__ void grid_barrier_arrive(const Params& p, const Shared& sm, int ct) {
-  named_bar_sync(1, GROUP_THREADS);  // every consumer thread's v stores precede the arrival
-  if (ct == 0) {
-    __threadfence();
-    if (atomicAdd(p.ctr + 8, 1) == (int)gridDim.x - 1) {
-      p.ctr[8] = 0;
-      __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ctr + 9), "r"(sm.grid_gen + 1) : "memory");
-    }
-  }
-}
-
-// One launch per lora_apply: phase 1 (shrink units) -> grid barrier -> phase 2 (expand
-// units).  MODE_SHRINK runs phase 1 only (v to v_out), MODE_EXPAND phase 2 only (v_in).
+// One launch per lora_apply: phase 1 (shrink units) then phase 2 (expand units) from one
+// CTA-local stream; an expand unit waits only for its own tile's shrink units (per-tile
+// counters), not for the whole grid.  MODE_SHRINK runs phase 1 only (v to v_out),
+// MODE_EXPAND phase 2 only (v_in).
 template <typename T>
-__global__ void __launch_bounds__(NTHREADS, 1) lora_apply_kernel(const __grid_constant__ Params p, int mode) {
+__global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __grid_constant__ Params p, int mode) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Shared& sm = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) sm.grid_gen = *reinterpret_cast<volatile int*>(p.ctr + 9);
   if (!prologue(p, sm)) {
     abort_launch(p);
     return;
@@ -918,14 +999,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_apply_kernel(const __grid_co
   const bool fused = mode == MODE_FUSED;
   // The producer is the highest-numbered warp: the SM's warp schedulers favour higher warp
   // ids, so the producer is never starved by the FMA-heavy consumer warps on its SMSP.
-  if (warp == GROUP_WARPS) {
+  if (warp == GROUP_WARPS + 1) {
+    // publisher: releases finished shrink units' v rows (tile counter += 1) in post order
+    if (lane == 0) {
+      for (int k = 0;; ++k) {
+        const int slot = k % PQ;
+        mbar_wait(&sm.pub_full[slot], (k / PQ) & 1);
+        int* c = sm.pub_slot[slot];
+        mbar_arrive(&sm.pub_empty[slot]);
+        if (!c) break;
+        __threadfence();  // cumulative: the consumers' v stores (acquired through pub_full)
+        atomicAdd(c, 1);
+      }
+    }
+  } else if (warp == GROUP_WARPS) {
     bool waited = false;
     int seq = 0;
     if (mode != MODE_EXPAND) seq = produce_shrink<T>(p, sm, seq, waited);
-    if (fused) {
-      if (lane == 0) post_marker(sm, seq, KIND_PHASE);
-      ++seq;
-    }
     if (mode != MODE_SHRINK) seq = produce_expand<T>(p, sm, seq, waited, fused);
     if (!waited) pdl_wait();
     if (lane == 0) post_marker(sm, seq, KIND_END);
@@ -933,24 +1023,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_apply_kernel(const __grid_co
     const int ct = tid;  // consumer warps 0 .. GROUP_WARPS-1
     const int gw = ct >> 5;
     float* red = reinterpret_cast<float*>(sm.scratch);
+    int npub = 0;  // consumer thread 0: tile counters posted to the publisher
     int seq = 0;
     for (;;) {
       const int stage = seq % NSTAGE;
       mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
       const Meta m0 = sm.meta[stage];
-      if (m0.kind == KIND_END) break;
-      if (m0.kind == KIND_PHASE) {
-        grid_barrier_arrive(p, sm, ct);
-        mbar_arrive(&sm.empty[stage]);
-        ++seq;
-        continue;
+      if (m0.kind == KIND_END) {
+        if (ct == 0) post_publish(sm, npub, nullptr);  // the publisher exits
+        break;
       }
       if (m0.kind == KIND_SHRINK) {
         switch (m0.T) {
-          case 1: shrink_unit<T, 1>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
-          case 2: shrink_unit<T, 2>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
-          case 3: shrink_unit<T, 3>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
-          default: shrink_unit<T, 4>(p, sm.plan, sm, seq, m0, red, ct, lane, gw); break;
+          case 1: shrink_unit<T, 1>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
+          case 2: shrink_unit<T, 2>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
+          case 3: shrink_unit<T, 3>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
+          default: shrink_unit<T, 4>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
         }
       } else {
         switch (m0.T) {
@@ -962,16 +1050,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) lora_apply_kernel(const __grid_co
       }
     }
   }
-  // the last CTA re-arms both unit counters for the next launch
+  // the last CTA re-arms the unit counters and the tile counters for the next launch
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+    sm.last_cta = atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (sm.last_cta) {
+    if (p.tile_ctr) {
+      const int n = p.n_jobs * sm.plan.totals[1];
+      for (int i = tid; i < n; i += APPLY_THREADS) p.tile_ctr[i] = 0;
+    }
+    if (tid == 0) {
       p.ctr[0] = 0;
       p.ctr[4] = 0;
       p.ctr[1] = 0;
-      __threadfence();
     }
+    __threadfence();
   }
 }
 
@@ -1012,11 +1108,14 @@ int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
   // counters ping-pong like the v buffer: apply n+1 may start (PDL) while apply n's last
   // CTA is still re-arming its own counter set
   prm.ctr = pool->d_ctr + 16 + (pool->apply_count & 1) * 16;
+  prm.tile_ctr = mode == MODE_FUSED ? pool->d_ctr + kTileCtrBase + (pool->apply_count & 1) * (size_t)kMaxJobs *
+                                                                      pool->max_tokens
+                                    : nullptr;
   prm.err = pool->d_ctr + 2;
   ++pool->apply_count;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pool->sm_count);
-  cfg.blockDim = dim3(NTHREADS);
+  cfg.blockDim = dim3(APPLY_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

@@ -164,6 +164,8 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_vws);
     cudaFree(pool->d_plan);
     cudaFree(pool->d_pws);
+    cudaFree(pool->d_pvimg);
+    cudaFree(pool->d_pctr);
     delete pool;
     cudaSetDevice(prev);
     return fail(code, msg);
@@ -180,7 +182,8 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   }
   e = cudaMalloc(&pool->d_slot_pages, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   if (e == cudaSuccess) e = cudaMalloc(&pool->d_slot_rank, sizeof(int) * (size_t)n_slots);
-  if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * 48);
+  const size_t n_ctr = cham::ctr_ints(max_tokens);
+  if (e == cudaSuccess) e = cudaMalloc(&pool->d_ctr, sizeof(int) * n_ctr);
   if (e == cudaSuccess)
     e = cudaMalloc(&pool->d_vws, 2 * sizeof(float) * (size_t)kMaxJobs * max_tokens * kMaxRank);
   if (e == cudaSuccess) {
@@ -189,10 +192,14 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   }
   if (e == cudaSuccess && pool->prefill_ok)
     e = cudaMalloc(&pool->d_pws, sizeof(float) * (size_t)kMaxJobs * kPrefillMaxSplit * max_tokens * kPrefillMaxRank);
+  if (e == cudaSuccess && pool->prefill_ok)
+    e = cudaMalloc(&pool->d_pvimg, (size_t)kMaxJobs * kPrefillMaxTiles * kPrefillVImg);
+  if (e == cudaSuccess && pool->prefill_ok) e = cudaMalloc(&pool->d_pctr, sizeof(int) * prefill_ctr_ints());
+  if (e == cudaSuccess && pool->prefill_ok) e = cudaMemset(pool->d_pctr, 0, sizeof(int) * prefill_ctr_ints());
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);
-  cudaMemset(pool->d_ctr, 0, sizeof(int) * 48);
+  cudaMemset(pool->d_ctr, 0, sizeof(int) * n_ctr);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cleanup(CHAM_ERR_CUDA, std::string("cham_pool_create: ") + cudaGetErrorString(e));
   cudaSetDevice(prev);
@@ -210,6 +217,8 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_vws);
   cudaFree(pool->d_plan);
   cudaFree(pool->d_pws);
+  cudaFree(pool->d_pvimg);
+  cudaFree(pool->d_pctr);
   delete pool;
   return CHAM_OK;
 }

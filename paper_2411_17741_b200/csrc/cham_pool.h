@@ -24,7 +24,8 @@ struct cham_pool {
   std::vector<int> slot_rank;          // host mirror
   std::vector<int> slot_pages;         // host mirror [n_slots][kMaxPagesPerSlot]
   // decode / shrink / expand workspace (one launch at a time per pool)
-  int* d_ctr = nullptr;                // [2] error; [16..31] / [32..47]: per-parity launch counters
+  int* d_ctr = nullptr;                // [2] error; [16..31] / [32..47]: per-parity launch counters;
+                                       // [64..): 2 x [kMaxJobs][max_tokens] per-tile v-ready counters
   float* d_vws = nullptr;              // 2 x [kMaxJobs][max_tokens][vws_kc][kMaxRank] (ping-pong)
   int vws_kc = 1;
   unsigned long long apply_count = 0;  // selects the v / counter ping-pong sets
@@ -38,12 +39,23 @@ struct cham_pool {
   int route_min_seg = 0;               // host hints about the next steps' segment lengths
   int route_max_seg = 1 << 30;
   float* d_pws = nullptr;              // prefill shrink partials [kMaxJobs][ks][max_tokens][128]
+  char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB]
+  int* d_pctr = nullptr;               // prefill counters: 2 parity sets + tile V flags
+  int prefill_epoch = 0;               // prefill launches so far (tile flags, counter parity)
 };
 
 namespace cham {
 constexpr int kPrefillMinTokens = 64;  // default routing threshold (segment tokens)
 constexpr int kPrefillMaxRank = 128;   // largest rank on the tcgen05 path (TMEM / smem budget)
 constexpr int kPrefillMaxSplit = 8;    // shrink split-K factor bound (workspace sizing)
+constexpr int kPrefillMaxTiles = 256;  // 128-row prefill tiles per apply (workspace sizing)
+constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles;  // one parity set: dispatch, done, spare, tile counters
+constexpr size_t kPrefillVImg = 32768;                // V image bytes per (job, tile)
+inline size_t prefill_ctr_ints() { return 2 * kPrefillCtrSet + kPrefillMaxTiles; }
+
+// d_ctr layout: launch counters, then the per-parity tile-ready counters of the decode kernel
+constexpr int kTileCtrBase = 64;
+inline size_t ctr_ints(int max_tokens) { return kTileCtrBase + 2 * (size_t)kMaxJobs * max_tokens; }
 
 // Threshold the plan and the launches use for this pool: segments with at least this many
 // tokens (and rank <= kPrefillMaxRank) go to the tcgen05 kernels.  INT_MAX = none.

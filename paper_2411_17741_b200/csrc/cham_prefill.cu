@@ -1,30 +1,31 @@
 // cham_prefill.cu — K3: the tensor-core (tcgen05) path for prefill-sized segments.
 //
 // Reference seam: the prefill half of CostModel.step_duration's LoRA term (engine.py:67-77):
-// a prefill contributes rank * input_tokens adapter units (engine.py:70, 75-76); these
-// kernels perform that work for real, y[t] += (x[t] . A_slot) . B_slot, for every segment
-// with at least `prefill_min_tokens` tokens (rank <= 128, bf16).
+// a prefill contributes rank * input_tokens adapter units (engine.py:70, 75-76); this kernel
+// performs that work for real, y[t] += (x[t] . A_slot) . B_slot, for every segment with at
+// least `prefill_min_tokens` tokens (rank <= 128, bf16).
 //
-// Two launches per lora_apply (K3):
-//  P1 shrink  unit = (job, 128-token tile, K-split):  D1[128 x rp] (TMEM, fp32) =
-//             X_tile[128 x K/ks] . A^T[rp x K/ks]^T.  X arrives by TMA tensor loads (one
-//             128-row box per 64-column stage when the tile's token rows are contiguous — the
-//             rows of a prefill request are — else one 1-row box per token: a TMA gather),
-//             A^T pages by 1 KiB bulk copies straight from the page layout, which already is
-//             the K-major SWIZZLE_128B canonical layout.  The epilogue writes fp32 partial
-//             v rows to a workspace (or, for the TP half, the final v to v_out).
-//  P2 expand  unit = (job, tile, 512 output columns):  V = sum of the K-split partials,
-//             rounded to bf16 into a K-major SWIZZLE_128B smem tile (zero beyond the rank);
-//             per 64-column group D2[128 x 64] (TMEM) = V . B with the B page slices used as
-//             MN-major SWIZZLE_128B operands (again the page layout itself); the y tile of the
-//             group is TMA-loaded into the same stage, and the epilogue adds D2 and stores the
-//             rows back — no separate elementwise kernel.
-// Both kernels are persistent (one CTA per SM) and warp-specialised: warps 0-3 epilogue
-// (TMEM lanes 0-127, one token row per thread), warp 4 loads (TMA), warp 5 issues the MMAs.
-// Stage rings are mbarrier pipelines; TMEM accumulators are double-buffered so the epilogue
-// of one unit overlaps the MMAs of the next.  The path is HBM-bound (AI ~15 flop/B at C3);
-// tensor cores are used because the CUDA-core FMA ceiling (~51-74 TFLOP/s) is below what the
-// HBM roofline demands.
+// ONE persistent, warp-specialised kernel per lora_apply (K3).  A tile is up to
+// 128 token rows of one segment (UMMA M = 128).  Units are dispatched dynamically from one
+// counter, phase-1 units first:
+//   shrink unit (tile, K-split kq, job group): D[128 x rp] (TMEM, fp32) = X . A^T over the
+//        unit's h_in range, for every job of the group from ONE x stage (q/k/v share x, so x
+//        crosses HBM->SM once per K range).  Stages carry kpc 64-column k-chunks: x by TMA
+//        tensor loads of exactly the tile's rows (32-row boxes, or 1-row boxes when the rows
+//        are not contiguous), A^T page atoms by 1 KiB bulk copies straight from the pool
+//        layout (K-major SWIZZLE_128B already).  The epilogue writes fp32 partial v rows; the
+//        last unit of a tile (split-K arrival counter) sums them and writes the tile's V image
+//        (bf16, K-major SWIZZLE_128B, exactly the UMMA A-operand layout) and publishes it
+//        (tile flag = launch epoch).
+//   expand unit (tile, job, 512 columns): the loader waits for the tile's V flag, copies the V
+//        image (one bulk copy), then streams 64-column groups: B page slices (MN-major
+//        SWIZZLE_128B — the pool layout again) + the y rows of the group.  D2[128 x 64] =
+//        V . B per group (double-buffered TMEM); the epilogue adds D2 to the y rows and stores
+//        them — no separate elementwise kernel.
+// Expand units wait only for their own tile, so the phases overlap.  Warps 0-3: epilogue (TMEM
+// lanes 0-127, one token row per thread); warp 4: loader (TMA + dispatch); warp 5: MMA issuer.
+// The path is HBM-bound (AI ~15 flop/B at C3): tensor cores are used because the CUDA-core
+// FMA ceiling (~51-74 TFLOP/s) is below what the HBM roofline demands.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -34,21 +35,21 @@ namespace cham {
 namespace prefill {
 
 constexpr int BM = 128;                 // tokens per tile (UMMA M)
-constexpr int BK = 64;                  // shrink K elements per stage (one 128-byte swizzle atom)
 constexpr int MAXR = kPrefillMaxRank;   // rank rows per adapter on this path
-constexpr int S1 = 6;                   // shrink ring stages
-constexpr int X_STAGE = BM * 128;       // 16 KiB
-constexpr int A_STAGE = MAXR * 128;     // 16 KiB (one 1 KiB atom per page)
-constexpr int BN = 64;                  // expand N per MMA group (one atom)
-constexpr int NSUB = 8;                 // expand groups per unit (512 columns)
-constexpr int S2 = 4;                   // expand ring stages
-constexpr int B_STAGE = MAXR * 128;     // 16 KiB
-constexpr int Y_STAGE = BM * 128;       // 16 KiB
-constexpr int V_TILE = BM * MAXR * 2;   // 32 KiB
-constexpr int NSEG = kMaxSegments;
+constexpr int NS = 4;                   // ring stages
+constexpr int STAGE = 32768;            // bytes per ring stage
+constexpr int VBUF = 2 * BM * 128;      // V image: <= 2 K-blocks x 128 rows x 128 B
+constexpr int CW = 512;                 // expand unit columns
+constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
+constexpr int UQ = 8;                   // unit-id ring depth
+constexpr int MAX_TILES = kPrefillMaxTiles;
 constexpr int NTHREADS = 192;           // warps 0-3 epilogue, 4 loader, 5 MMA
-constexpr int P1_TMEM = 256;            // two 128-column fp32 accumulators
-constexpr int P2_TMEM = 128;            // two 64-column fp32 accumulators
+constexpr int TMEM_COLS = 512;
+constexpr int TM_SH = 192;              // shrink accumulator stride: [0,192) and [192,384)
+constexpr int TM_EX = 384;              // expand accumulators: [384,448) and [448,512)
+constexpr int BAR_EPI = 1;              // named barrier of the 128 epilogue threads
+
+enum Mode { MODE_FUSED = 0, MODE_SHRINK = 1, MODE_EXPAND = 2 };
 
 struct Job {
   const char* x;
@@ -57,34 +58,40 @@ struct Job {
   long long b_off;
 };
 
-// Activation tensor maps of one job (x for P1, y for P2): a 64-column x 128-row box for
-// contiguous tiles and a 64-column x 1-row box for gathered ones, both SWIZZLE_128B.
+// Activation tensor maps of one job: a 64-column x 32-row box for contiguous rows and a
+// 64-column x 1-row box for gathered ones, both SWIZZLE_128B (x for shrink, y for expand).
 struct alignas(64) Maps {
-  CUtensorMap tile;
-  CUtensorMap row;
+  CUtensorMap x32, x1, y32, y1;
 };
 
 struct alignas(64) Params {
   Maps maps[kMaxJobs];
+  Job jobs[kMaxJobs];
   const char* base;
   long long page_bytes;
   const int* slot_pages;
   int h_in, h_out;
   int n_jobs;
-  Job jobs[kMaxJobs];
+  int mode;
+  int x_shared;            // every job reads the same x (q/k/v): one x stage serves the group
   const int* perm;
   const int* seg_off;
   const int* seg_slot;
   const int* seg_rank;
   int n_seg;
   const int* n_seg_dev;
-  int thr;             // routing threshold (segment tokens)
-  int grid1;           // P1 grid size (the K-split factor is derived from it)
-  int split_ok;        // 0: no K-split (TP shrink writes final v)
-  float* vout;         // P1 output: [job][ks][pos][ld]
-  const float* vin;    // P2 input
-  long long v_job_stride, v_ks_stride;
-  int ld;              // floats per v row
+  int thr;                 // routing threshold (segment tokens)
+  int epoch;               // launch id (tile V flags), parity selects the counter set
+  int* ctr;                // this parity's counters: [0] dispatch, [1] finished CTAs, [2] error
+  int* tile_cnt;           // this parity's split-K arrival counters [MAX_TILES]
+  int* vready;             // [MAX_TILES] tile V flags (= epoch when the V images are final)
+  int* err;
+  float* part;             // fp32 shrink partials [job][kq][position][MAXR]
+  long long part_job, part_ks;
+  char* vimg;              // V images [job][tile][VBUF]
+  float* v_out;            // MODE_SHRINK: v [position][v_stride]
+  const float* v_in;       // MODE_EXPAND: v [position][v_stride]
+  int v_stride;
 };
 
 // ------------------------------------------------------------------ PTX wrappers (tcgen05)
@@ -111,14 +118,13 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "n"(COLS));
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+               "n"(TMEM_COLS));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
 }
-template <int COLS>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(COLS));
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(TMEM_COLS));
 }
 // 32 lanes x 32 consecutive fp32 columns: thread `lane` of the warp gets row (lane base + lane)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -148,454 +154,664 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
-__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {  // 16-byte chunk of a 128-byte row
   return (uint32_t)(row * 128 + (((chunk ^ row) & 7) << 4));
 }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// ------------------------------------------------------------------ tile list (per CTA)
+// ------------------------------------------------------------------ tiles and units
+struct Tile {
+  int pos0;  // first position (perm order) of the tile's rows
+  int m;     // rows (<= 128)
+  int slot;
+  int rank;
+};
 struct TileList {
   int n_tiles;
-  int n_pseg;
-  int pseg[NSEG];          // prefill segment -> segment index
-  int tstart[NSEG + 1];    // tile prefix over prefill segments
-  int s_off[NSEG];
-  int s_T[NSEG];
-  int s_slot[NSEG];
-  int s_rank[NSEG];
+  int ks;           // shrink K-split factor
+  int u1;           // phase-1 units
+  int u_total;
+  int sh_start[MAX_TILES + 1];
+  Tile t[MAX_TILES];
 };
 
-// All threads: read the segment table into smem, compact the prefill segments (stable),
-// prefix their 128-token tile counts.  Deterministic: P1 and P2 derive the same list.
-__device__ void build_tiles(const Params& p, TileList& tl) {
-  const int tid = threadIdx.x, lane = tid & 31;
+__host__ __device__ __forceinline__ int rpad(int rank) { return (rank + 15) & ~15; }
+__host__ __device__ __forceinline__ int mpad(int m) { return (m + 31) & ~31; }
+// jobs sharing one shrink stage: all of them when their A^T atoms fit a 16 KiB region
+__device__ __forceinline__ int jobs_per_group(const Params& p, int rank) {
+  return (p.mode == MODE_FUSED && p.x_shared && p.n_jobs * (rpad(rank) / 8) <= 16) ? p.n_jobs : 1;
+}
+__device__ __forceinline__ int n_groups(const Params& p, int rank) { return p.n_jobs / jobs_per_group(p, rank); }
+
+// Warp 0 of every CTA builds the same tile list (deterministic): prefill segments in table
+// order, each cut into 128-row tiles; phase-1 unit prefix per tile.  Returns false on overflow.
+__device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
+  const int lane = threadIdx.x & 31;
   int S = p.n_seg >= 0 ? p.n_seg : *p.n_seg_dev;
-  S = max(0, min(S, NSEG));
-  for (int s = tid; s < S; s += blockDim.x) {
-    const int o0 = __ldg(p.seg_off + s), o1 = __ldg(p.seg_off + s + 1);
-    tl.s_off[s] = o0;
-    tl.s_T[s] = o1 - o0;
-    tl.s_slot[s] = __ldg(p.seg_slot + s);
-    tl.s_rank[s] = __ldg(p.seg_rank + s);
-  }
-  __syncthreads();
-  if (tid < 32) {
-    int cnt = 0, tiles = 0;
-    for (int base = 0; base < S; base += 32) {
-      const int s = base + lane;
-      const bool f = s < S && tl.s_slot[s] >= 0 && is_prefill_segment(tl.s_T[s], tl.s_rank[s], p.thr);
-      const unsigned m = __ballot_sync(0xffffffffu, f);
-      const int nt = f ? (tl.s_T[s] + BM - 1) / BM : 0;
-      int inc = nt;
+  S = max(0, min(S, kMaxSegments));
+  int tiles = 0;
+  bool ok = true;
+  for (int base = 0; base < S; base += 32) {
+    const int s = base + lane;
+    int o0 = 0, T = 0, slot = -1, rank = 0;
+    if (s < S) {
+      o0 = __ldg(p.seg_off + s);
+      T = __ldg(p.seg_off + s + 1) - o0;
+      slot = __ldg(p.seg_slot + s);
+      rank = __ldg(p.seg_rank + s);
+    }
+    const bool f = s < S && slot >= 0 && is_prefill_segment(T, rank, p.thr);
+    const int nt = f ? (T + BM - 1) / BM : 0;
+    int inc = nt;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += a;
-      }
-      if (f) {
-        const int i = cnt + __popc(m & ((1u << lane) - 1));
-        tl.pseg[i] = s;
-        tl.tstart[i] = tiles + inc - nt;
-      }
-      cnt += __popc(m);
-      tiles += __shfl_sync(0xffffffffu, inc, 31);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
     }
-    if (lane == 0) {
-      tl.n_pseg = cnt;
-      tl.n_tiles = tiles;
-      tl.tstart[cnt] = tiles;
-    }
+    const int first = tiles + inc - nt;
+    if (first + nt > MAX_TILES) ok = false;
+    else
+      for (int i = 0; i < nt; ++i) {
+        Tile t;
+        t.pos0 = o0 + i * BM;
+        t.m = min(BM, T - i * BM);
+        t.slot = slot;
+        t.rank = rank;
+        tl.t[first + i] = t;
+      }
+    tiles += __shfl_sync(0xffffffffu, inc, 31);
   }
-  __syncthreads();
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok) return false;
+  // K-split: about two phase-1 units per CTA, K loops of >= 8 chunks
+  const int nkc = p.h_in / 64;
+  int groups = 0;
+  for (int t = lane; t < tiles; t += 32) groups += n_groups(p, tl.t[t].rank);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) groups += __shfl_xor_sync(0xffffffffu, groups, o);
+  int ks = 1;
+  if (p.mode == MODE_FUSED)
+    while (ks < kPrefillMaxSplit && groups * ks < 2 * grid && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8) ks *= 2;
+  // phase-1 unit prefix (vbuild units in MODE_EXPAND: one per tile)
+  int carry = 0;
+  for (int base = 0; base < tiles; base += 32) {
+    const int t = base + lane;
+    const int u = t < tiles ? (p.mode == MODE_EXPAND ? 1 : ks * n_groups(p, tl.t[t].rank)) : 0;
+    int inc = u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    if (t < tiles) tl.sh_start[t] = carry + inc - u;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) {
+    tl.n_tiles = tiles;
+    tl.ks = ks;
+    tl.sh_start[tiles] = carry;
+    tl.u1 = carry;
+    const int ncc = (p.h_out + CW - 1) / CW;
+    tl.u_total = carry + (p.mode == MODE_SHRINK ? 0 : tiles * p.n_jobs * ncc);
+  }
+  return true;
 }
 
-// prefill-segment index owning tile t
-__device__ __forceinline__ int tile_pseg(const TileList& tl, int t) {
-  int lo = 0, hi = tl.n_pseg;
+__device__ __forceinline__ int tile_of_unit(const TileList& tl, int u) {
+  int lo = 0, hi = tl.n_tiles;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (tl.tstart[mid] <= t) lo = mid; else hi = mid;
+    if (tl.sh_start[mid] <= u) lo = mid; else hi = mid;
   }
   return lo;
 }
 
-__device__ __forceinline__ int choose_ks(const Params& p, int n_tiles) {
-  const int nkc = p.h_in / BK;
-  if (!p.split_ok) return 1;
-  int ks = 1;
-  // about four units per CTA: balances the tail without shrinking the K loops below 8 stages
-  while (ks < kPrefillMaxSplit && n_tiles * p.n_jobs * ks < 4 * p.grid1 && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8)
-    ks *= 2;
-  return ks;
-}
-
+// Everything every role derives from a unit id.
 struct Unit {
-  int job, seg, row0, m, rank, rp, np, slot;
+  int kind;    // 1 shrink, 2 expand, 3 vbuild (MODE_EXPAND phase 1)
+  int tile, pos0, m, mp, slot, rank, rp, np;
+  int kq, job0, jps;  // shrink: K range, first job, jobs in the group
+  int job, col0;      // expand
+  int ngrp;           // expand: 64-column groups in the unit
+  int kpc, nst;       // chunks (shrink) / groups (expand) per stage, stages
+  int nchunks;        // shrink: k-chunks in the unit
+  int xb;             // bytes of one activation chunk/group in smem (mp rows x 128 B)
+  int bstride;        // expand: bytes of one group's B slices (np rounded up to even, x 1 KiB)
 };
-__device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, int job, int t) {
-  Unit u;
-  const int i = tile_pseg(tl, t);
-  u.job = job;
-  u.seg = tl.pseg[i];
-  const int tile_in_seg = t - tl.tstart[i];
-  u.row0 = tl.s_off[u.seg] + tile_in_seg * BM;
-  u.m = min(BM, tl.s_T[u.seg] - tile_in_seg * BM);
-  u.rank = tl.s_rank[u.seg];
-  u.rp = (u.rank + 15) & ~15;
-  u.np = (u.rank + kRowsPerPage - 1) / kRowsPerPage;
-  u.slot = tl.s_slot[u.seg];
-  return u;
-}
 
-// Token rows of a unit's tile as seen by the loader warp: lane l holds rows l, l+32, l+64,
-// l+96 (perm applied); `contig` = the m rows are consecutive (one TMA box per stage).
-struct TileRows {
-  int row[4];
-  int first;
-  bool contig;
-};
-__device__ __forceinline__ TileRows tile_rows(const Params& p, int row0, int m, int lane) {
-  TileRows t;
-  bool ok = true;
-  t.first = p.perm ? __ldg(p.perm + row0) : row0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = lane + 32 * i;
-    const int pos = row0 + min(r, m - 1);
-    t.row[i] = p.perm ? __ldg(p.perm + pos) : pos;
-    if (r < m) ok &= t.row[i] == t.first + r;
-  }
-  t.contig = __all_sync(0xffffffffu, ok);
-  return t;
-}
-
-// Loader-warp helper: one activation stage (64 columns at c0) of the tile into smem.
-__device__ __forceinline__ void load_act(const Maps& mp, const TileRows& tr, int m, int c0, unsigned char* dst,
-                                         uint64_t* bar, uint64_t pol, int lane) {
-  if (tr.contig) {
-    if (lane == 0) tma_load_2d(dst, &mp.tile, c0, tr.first, bar, pol);
+__device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, int u) {
+  Unit x;
+  if (u < tl.u1) {
+    x.tile = tile_of_unit(tl, u);
+    x.kind = p.mode == MODE_EXPAND ? 3 : 1;
   } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = lane + 32 * i;
-      if (r < m) tma_load_2d(dst + r * 128, &mp.row, c0, tr.row[i], bar, pol);
-    }
+    const int ncc = (p.h_out + CW - 1) / CW;
+    const int r = u - tl.u1;
+    x.tile = r / (p.n_jobs * ncc);
+    const int jc = r - x.tile * p.n_jobs * ncc;
+    x.job = jc / ncc;
+    x.col0 = (jc - x.job * ncc) * CW;
+    x.kind = 2;
   }
+  const Tile& t = tl.t[x.tile];
+  x.pos0 = t.pos0;
+  x.m = t.m;
+  x.mp = mpad(t.m);
+  x.slot = t.slot;
+  x.rank = t.rank;
+  x.rp = rpad(t.rank);
+  x.np = (t.rank + 7) / 8;
+  x.xb = x.mp * 128;
+  x.bstride = (x.rp / 8) * kAtomBytes;
+  if (x.kind == 1) {
+    const int rem = u - tl.sh_start[x.tile];
+    x.kq = rem % tl.ks;
+    x.jps = jobs_per_group(p, t.rank);
+    x.job0 = (rem / tl.ks) * x.jps;
+    x.nchunks = (p.h_in / 64) / tl.ks;
+    const int chunk_bytes = x.xb + x.jps * (x.rp / 8) * kAtomBytes;
+    x.kpc = max(1, min(4, min(STAGE / chunk_bytes, x.nchunks)));
+    x.nst = (x.nchunks + x.kpc - 1) / x.kpc;
+  } else if (x.kind == 2) {
+    x.ngrp = min(NGRP, (p.h_out - x.col0) / 64);
+    x.kpc = max(1, min(4, STAGE / (x.bstride + x.xb)));
+    x.nst = (x.ngrp + x.kpc - 1) / x.kpc;
+  } else {
+    x.kpc = 0;
+    x.nst = 0;
+  }
+  return x;
 }
-__device__ __forceinline__ uint32_t act_bytes(const TileRows& tr, int m) { return tr.contig ? BM * 128 : m * 128; }
 
-// =========================================================================== P1: shrink
-struct P1Shared {
-  alignas(1024) unsigned char x[S1][X_STAGE];
-  alignas(1024) unsigned char a[S1][A_STAGE];
-  uint64_t full[S1], empty[S1], tfull[2], tempty[2];
+// Token rows of one 32-row block of a tile as seen by a loader lane: the block is contiguous
+// when its rows are consecutive tokens (one TMA box), else each lane loads its own row.
+__device__ __forceinline__ int block_row(const Params& p, const Unit& u, int blk, int lane, bool& contig) {
+  const int r = blk * 32 + lane;
+  const int pos = u.pos0 + min(r, u.m - 1);
+  const int row = p.perm ? __ldg(p.perm + pos) : pos;
+  const int first = __shfl_sync(0xffffffffu, row, 0);
+  contig = __all_sync(0xffffffffu, r >= u.m || row == first + lane);
+  return row;
+}
+
+// ------------------------------------------------------------------ shared memory
+struct Shared {
+  alignas(1024) unsigned char ring[NS][STAGE];
+  alignas(1024) unsigned char vbuf[2][VBUF];
+  uint64_t full[NS], empty[NS];
+  uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[2], tempty_ex[2];
+  uint64_t vfull[2], vempty[2];
+  uint64_t ufull[UQ], uempty[UQ];
+  int uslot[UQ];
   uint32_t tmem_base;
+  int last;
+  int flag;
   TileList tl;
 };
 
-__global__ void __launch_bounds__(NTHREADS, 1) shrink_kernel(const __grid_constant__ Params p) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  P1Shared& sm = *reinterpret_cast<P1Shared*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    for (int i = 0; i < S1; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 128);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 4 && lane < p.n_jobs) {
-    prefetch_map(&p.maps[lane].tile);
-    prefetch_map(&p.maps[lane].row);
-  }
-  if (warp == 5) {
-    tmem_alloc<P1_TMEM>(&sm.tmem_base);
-    tc_fence_before();
-  }
-  build_tiles(p, sm.tl);  // contains __syncthreads
-  tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
-  const int n_tiles = sm.tl.n_tiles;
-  const int ks = choose_ks(p, n_tiles);
-  const int nkc = p.h_in / BK / ks;  // stages per unit
-  const int n_units = n_tiles * ks * p.n_jobs;
-
-  if (warp == 4) {
-    // ---------------- loader: X by TMA tensor loads, A^T by 1 KiB page bulk copies
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();  // the other jobs of the tile re-read x from L2
-    int seq = 0;
-    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x) {
-      const int job = uu % p.n_jobs, rem = uu / p.n_jobs;
-      const Unit u = make_unit(p, sm.tl, job, rem / ks);
-      const int kq = rem % ks;
-      const TileRows tr = tile_rows(p, u.row0, u.m, lane);
-      const char* blk0 = p.base + p.jobs[job].a_off;
-      const long long pg = lane < u.np ? (long long)__ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + lane) : 0;
-      const uint32_t bytes = act_bytes(tr, u.m) + u.np * kAtomBytes;
-      for (int k = 0; k < nkc; ++k, ++seq) {
-        const int st = seq % S1;
-        if (seq >= S1) mbar_wait(&sm.empty[st], ((seq / S1) - 1) & 1);
-        if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
-        __syncwarp();
-        const int kc = kq * nkc + k;
-        load_act(p.maps[job], tr, u.m, kc * BK, sm.x[st], &sm.full[st], pol_x, lane);
-        if (lane < u.np)
-          bulk_g2s(sm.a[st] + lane * kAtomBytes, blk0 + pg * p.page_bytes + (long long)kc * kAtomBytes, kAtomBytes,
-                   &sm.full[st], pol_w);
-      }
-    }
-  } else if (warp == 5) {
-    // ---------------- MMA issuer
-    int seq = 0, ui = 0;
-    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
-      const int job = uu % p.n_jobs, rem = uu / p.n_jobs;
-      const Unit u = make_unit(p, sm.tl, job, rem / ks);
-      const int acc = ui & 1;
-      if (ui >= 2) mbar_wait(&sm.tempty[acc], ((ui >> 1) - 1) & 1);
-      tc_fence_after();
-      const uint32_t idesc = idesc_bf16(BM, u.rp, false);
-      const uint32_t d = tmem + acc * 128;
-      for (int k = 0; k < nkc; ++k, ++seq) {
-        const int st = seq % S1;
-        mbar_wait(&sm.full[st], (seq / S1) & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t xa = smem_u32(sm.x[st]), aa = smem_u32(sm.a[st]);
+// V image of (job, tile): K-block b (64 ranks) of row r, 16-byte chunk c at
+// b * mp*128 + r*128 + ((c ^ r) & 7) * 16 — the K-major SWIZZLE_128B A-operand layout.
+__device__ __forceinline__ char* vimg_of(const Params& p, int job, int tile) {
+  return p.vimg + ((long long)job * MAX_TILES + tile) * VBUF;
+}
+// ranks [c0, c0 + 32) of row r (v[i] = rank c0 + i; ranks >= nvals are written as zero),
+// clipped to the rp columns of the image
+__device__ __forceinline__ void write_v_chunk(char* img, const Unit& u, int r, int c0, const float (&v)[32],
+                                              int nvals) {
 #pragma unroll
-          for (int j = 0; j < BK / 16; ++j) {
-            const uint64_t ad = sdesc(xa + j * 32, 16, 1024);
-            const uint64_t bd = sdesc(aa + j * 32, 16, kAtomBytes);
-            mma_bf16(d, ad, bd, idesc, (k | j) ? 1u : 0u);
-          }
-          mma_commit(&sm.empty[st]);
-          if (k == nkc - 1) mma_commit(&sm.tfull[acc]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ---------------- epilogue warps 0-3: TMEM -> fp32 partial v rows
-    int ui = 0;
-    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
-      const int job = uu % p.n_jobs, rem = uu / p.n_jobs;
-      const Unit u = make_unit(p, sm.tl, job, rem / ks);
-      const int kq = rem % ks;
-      const int acc = ui & 1;
-      mbar_wait(&sm.tfull[acc], (ui >> 1) & 1);
-      tc_fence_after();
-      const int r = warp * 32 + lane;
-      float* dst = p.vout + job * p.v_job_stride + kq * p.v_ks_stride + (long long)(u.row0 + r) * p.ld;
-      for (int c0 = 0; c0 < u.rank; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + acc * 128 + c0 + ((uint32_t)(warp * 32) << 16), v);
-        if (r < u.m) {
+  for (int q = 0; q < 4; ++q) {
+    const int c8 = (c0 >> 3) + q;
+    if (c8 * 8 < u.rp) {
+      float f[8];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            if (c0 + i < u.rank) *reinterpret_cast<float4*>(dst + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&sm.tempty[acc]);
+      for (int i = 0; i < 8; ++i) f[i] = c0 + q * 8 + i < nvals ? v[q * 8 + i] : 0.f;
+      const uint4 w = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                 pack_bf16x2(f[6], f[7]));
+      *reinterpret_cast<uint4*>(img + (c8 >> 3) * u.xb + swz(r, c8 & 7)) = w;
     }
-  }
-  __syncthreads();
-  if (warp == 5) {
-    tc_fence_after();
-    tmem_dealloc<P1_TMEM>(tmem);
   }
 }
 
-// =========================================================================== P2: expand
-struct P2Shared {
-  alignas(1024) unsigned char v[2][V_TILE];
-  alignas(1024) unsigned char b[S2][B_STAGE];
-  alignas(1024) unsigned char y[S2][Y_STAGE];
-  uint64_t full[S2], empty[S2], vfull[2], vempty[2], tfull[2], tempty[2];
-  uint32_t tmem_base;
-  TileList tl;
-};
+// Epilogue: the tile's V images are final -> publish the tile flag (release).
+__device__ __forceinline__ void publish_tile(const Params& p, int tile, int et) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // this thread's V stores -> TMA reads
+  named_bar_sync(BAR_EPI, 128);
+  if (et == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.vready + tile), "r"(p.epoch) : "memory");
+  }
+}
 
-__global__ void __launch_bounds__(NTHREADS, 1) expand_kernel(const __grid_constant__ Params p) {
+// =========================================================================== the kernel
+__global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  P2Shared& sm = *reinterpret_cast<P2Shared*>(smem_raw);
+  Shared& sm = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < S2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 1 + 128);  // MMA commit (B read) + 128 epilogue threads (y read)
+      mbar_init(&sm.empty[i], 1 + 4);  // MMA commit + one arrival per epilogue warp
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.vfull[i], 128);
+      mbar_init(&sm.tfull_sh[i], 1);
+      mbar_init(&sm.tempty_sh[i], 4);
+      mbar_init(&sm.tfull_ex[i], 1);
+      mbar_init(&sm.tempty_ex[i], 4);
+      mbar_init(&sm.vfull[i], 1);
       mbar_init(&sm.vempty[i], 1);
-      mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 128);
+    }
+    for (int i = 0; i < UQ; ++i) {
+      mbar_init(&sm.ufull[i], 1);
+      mbar_init(&sm.uempty[i], 1 + 4);
     }
     fence_mbar_init();
   }
   if (warp == 4 && lane < p.n_jobs) {
-    prefetch_map(&p.maps[lane].tile);
-    prefetch_map(&p.maps[lane].row);
+    prefetch_map(&p.maps[lane].x32);
+    prefetch_map(&p.maps[lane].x1);
+    prefetch_map(&p.maps[lane].y32);
+    prefetch_map(&p.maps[lane].y1);
   }
   if (warp == 5) {
-    tmem_alloc<P2_TMEM>(&sm.tmem_base);
+    tmem_alloc(&sm.tmem_base);
     tc_fence_before();
   }
-  build_tiles(p, sm.tl);
+  if (warp == 0) sm.flag = build_tiles(p, sm.tl, gridDim.x) ? 1 : 0;
+  __syncthreads();
   tc_fence_after();
+  const TileList& tl = sm.tl;
   const uint32_t tmem = sm.tmem_base;
-  const int n_tiles = sm.tl.n_tiles;
-  const int ks = choose_ks(p, n_tiles);
-  const int ncols_unit = NSUB * BN;
-  const int nq = (p.h_out + ncols_unit - 1) / ncols_unit;
-  const int n_units = n_tiles * nq * p.n_jobs;
-
-  if (warp == 4) {
-    // ---------------- loader: per 64-column group, one 1 KiB B slice per page + the y tile
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_y = policy_evict_last();  // written back right after
-    int seq = 0;
-    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x) {
-      const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
-      const Unit u = make_unit(p, sm.tl, job, rem / nq);
-      const int n0 = (rem % nq) * ncols_unit;
-      const int nsub = min(NSUB, (p.h_out - n0) / BN);
-      const TileRows tr = tile_rows(p, u.row0, u.m, lane);
-      const char* blk0 = p.base + p.jobs[job].b_off;
-      const long long pg = lane < u.np ? (long long)__ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + lane) : 0;
-      const bool pad = u.rp / kRowsPerPage > u.np;  // odd page count: zero pad page (K rows rank..rp)
-      const uint32_t bytes = act_bytes(tr, u.m) + u.np * kAtomBytes;
-      for (int c = 0; c < nsub; ++c, ++seq) {
-        const int st = seq % S2;
-        if (seq >= S2) mbar_wait(&sm.empty[st], ((seq / S2) - 1) & 1);
-        if (pad) {
-          uint4* z = reinterpret_cast<uint4*>(sm.b[st] + u.np * kAtomBytes);
-          z[lane] = make_uint4(0, 0, 0, 0);
-          z[lane + 32] = make_uint4(0, 0, 0, 0);
-          fence_proxy_async_shared();
+  pdl_wait();  // x, y, v and the workspaces may belong to the previous kernel
+  pdl_launch_dependents();
+  if (!sm.flag) {
+    if (tid == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- loader + dispatch
+    const uint64_t pol_w = policy_evict_first();  // adapter pages: streamed
+    const uint64_t pol_x = policy_evict_last();   // x: re-read by the other job groups / K ranges
+    const uint64_t pol_y = policy_evict_first();
+    int next = blockIdx.x;  // first unit static, the rest from the counter (one claim ahead)
+    int claim = 0;
+    if (lane == 0 && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
+    // tile V flag of an expand unit, read without blocking one unit ahead
+    const int ex_per_tile = p.n_jobs * ((p.h_out + CW - 1) / CW);
+    auto peek_flag = [&](int u) {
+      int v = 0;
+      if (lane == 0 && u >= tl.u1 && u < tl.u_total) {
+        const int* f = p.vready + (u - tl.u1) / ex_per_tile;
+        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      }
+      return v;
+    };
+    int flag = peek_flag(next);
+    int seq = 0, nex = 0;
+    for (int k = 0;; ++k) {
+      const int u_id = __shfl_sync(0xffffffffu, next < tl.u_total ? next : -1, 0);
+      // publish the unit id to the MMA and epilogue warps
+      const int q = k % UQ;
+      if (lane == 0) {
+        if (k >= UQ) mbar_wait(&sm.uempty[q], ((k / UQ) - 1) & 1);
+        sm.uslot[q] = u_id;
+        mbar_arrive(&sm.ufull[q]);
+      }
+      if (u_id < 0) break;
+      next = __shfl_sync(0xffffffffu, claim, 0) + gridDim.x;
+      if (lane == 0 && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
+      const int cur_flag = flag;
+      flag = peek_flag(next);
+      const Unit u = make_unit(p, tl, u_id);
+      if (u.kind == 3) continue;
+      const int my_page = lane < u.np ? __ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + lane) : 0;
+      if (u.kind == 1) {
+        // ---- shrink: x chunks of the tile + A^T atoms of every job of the group
+        const int nblk = (u.m + 31) / 32;
+        bool contig[4];
+        int rows[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(p, u, b, lane, contig[b]) : 0;
+        const int kc0 = u.kq * u.nchunks;
+        const int n_cp = u.jps * u.np;  // A copies per chunk
+        for (int s = 0; s < u.nst; ++s, ++seq) {
+          const int st = seq % NS;
+          const int c_first = s * u.kpc;
+          const int nch = min(u.kpc, u.nchunks - c_first);
+          if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
+          uint32_t bytes = nch * n_cp * kAtomBytes;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (b < nblk) bytes += nch * (contig[b] ? 32 * 128 : min(32, u.m - b * 32) * 128);
+          if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
+          __syncwarp();
+          unsigned char* stg = sm.ring[st];
+          for (int i = 0; i < nch; ++i) {
+            const int kc = kc0 + c_first + i;
+            unsigned char* xdst = stg + i * u.xb;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b >= nblk) continue;
+              if (contig[b]) {
+                if (lane == 0)
+                  tma_load_2d(xdst + b * 32 * 128, &p.maps[u.job0].x32, kc * 64, rows[b], &sm.full[st], pol_x);
+              } else if (b * 32 + lane < u.m) {
+                tma_load_2d(xdst + (b * 32 + lane) * 128, &p.maps[u.job0].x1, kc * 64, rows[b], &sm.full[st], pol_x);
+              }
+            }
+            unsigned char* adst = stg + u.kpc * u.xb + i * u.jps * u.bstride;
+            // lanes 0..np-1 hold the page ids; copy job by job
+            for (int j = 0; j < u.jps; ++j) {
+              if (lane < u.np) {
+                const char* src = p.base + (long long)my_page * p.page_bytes + p.jobs[u.job0 + j].a_off +
+                                  (long long)kc * kAtomBytes;
+                bulk_g2s(adst + j * u.bstride + lane * kAtomBytes, src, kAtomBytes, &sm.full[st], pol_w);
+              }
+            }
+          }
+        }
+      } else {
+        // ---- expand: V image of (job, tile), then B slices + y rows per 64-column group
+        const int vb = nex & 1;
+        if (lane == 0) {
+          if (nex >= 2) mbar_wait(&sm.vempty[vb], ((nex >> 1) - 1) & 1);
+          if (cur_flag != p.epoch)
+            while (ld_acquire_gpu(p.vready + u.tile) != p.epoch) __nanosleep(32);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const uint32_t vbytes = ((u.rp + 63) / 64) * u.xb;
+          mbar_arrive_expect_tx(&sm.vfull[vb], vbytes);
+          bulk_g2s(sm.vbuf[vb], vimg_of(p, u.job, u.tile), vbytes, &sm.vfull[vb], pol_w);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
-        __syncwarp();
-        const int col = n0 + c * BN;
-        if (lane < u.np)
-          bulk_g2s(sm.b[st] + lane * kAtomBytes, blk0 + pg * p.page_bytes + (long long)(col / 64) * kAtomBytes,
-                   kAtomBytes, &sm.full[st], pol_w);
-        load_act(p.maps[job], tr, u.m, col, sm.y[st], &sm.full[st], pol_y, lane);
+        ++nex;
+        const int nblk = (u.m + 31) / 32;
+        bool contig[4];
+        int rows[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(p, u, b, lane, contig[b]) : 0;
+        const bool pad = (u.rp / 8) > u.np;
+        for (int s = 0; s < u.nst; ++s, ++seq) {
+          const int st = seq % NS;
+          const int g_first = s * u.kpc;
+          const int ng = min(u.kpc, u.ngrp - g_first);
+          if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
+          unsigned char* stg = sm.ring[st];
+          if (pad) {
+            // odd page count: the K rows rank..rp of every group are a zero atom
+            for (int g = 0; g < ng; ++g) {
+              uint4* z = reinterpret_cast<uint4*>(stg + g * u.bstride + u.np * kAtomBytes);
+              z[lane] = make_uint4(0, 0, 0, 0);
+              z[lane + 32] = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_shared();
+          }
+          __syncwarp();
+          uint32_t bytes = ng * u.np * kAtomBytes;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (b < nblk) bytes += ng * (contig[b] ? 32 * 128 : min(32, u.m - b * 32) * 128);
+          if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
+          __syncwarp();
+          for (int g = 0; g < ng; ++g) {
+            const int col = u.col0 + (g_first + g) * 64;
+            if (lane < u.np) {
+              const char* src = p.base + (long long)my_page * p.page_bytes + p.jobs[u.job].b_off +
+                                (long long)(col / 64) * kAtomBytes;
+              bulk_g2s(stg + g * u.bstride + lane * kAtomBytes, src, kAtomBytes, &sm.full[st], pol_w);
+            }
+            unsigned char* ydst = stg + u.kpc * u.bstride + g * u.xb;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b >= nblk) continue;
+              if (contig[b]) {
+                if (lane == 0) tma_load_2d(ydst + b * 32 * 128, &p.maps[u.job].y32, col, rows[b], &sm.full[st], pol_y);
+              } else if (b * 32 + lane < u.m) {
+                tma_load_2d(ydst + (b * 32 + lane) * 128, &p.maps[u.job].y1, col, rows[b], &sm.full[st], pol_y);
+              }
+            }
+          }
+        }
       }
     }
   } else if (warp == 5) {
-    // ---------------- MMA issuer
-    int seq = 0, gi = 0, ui = 0;
-    const uint32_t idesc = idesc_bf16(BM, BN, true);
-    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
-      const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
-      const Unit u = make_unit(p, sm.tl, job, rem / nq);
-      const int n0 = (rem % nq) * ncols_unit;
-      const int nsub = min(NSUB, (p.h_out - n0) / BN);
-      const int vb = ui & 1;
-      mbar_wait(&sm.vfull[vb], (ui >> 1) & 1);
-      tc_fence_after();
-      for (int c = 0; c < nsub; ++c, ++seq, ++gi) {
-        const int st = seq % S2, acc = gi & 1;
-        if (gi >= 2) mbar_wait(&sm.tempty[acc], ((gi >> 1) - 1) & 1);
-        mbar_wait(&sm.full[st], (seq / S2) & 1);
+    // ---------------------------------------------------------------- MMA issuer
+    int seq = 0, nsh = 0, nex = 0, ngrp = 0;
+    const uint32_t idesc_ex = idesc_bf16(BM, 64, true);
+    for (int k = 0;; ++k) {
+      const int q = k % UQ;
+      mbar_wait(&sm.ufull[q], (k / UQ) & 1);
+      const int u_id = sm.uslot[q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.uempty[q]);
+      if (u_id < 0) break;
+      const Unit u = make_unit(p, tl, u_id);
+      if (u.kind == 3) continue;
+      if (u.kind == 1) {
+        const int ab = nsh & 1;
+        if (nsh >= 2) mbar_wait(&sm.tempty_sh[ab], ((nsh >> 1) - 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t va = smem_u32(sm.v[vb]), ba = smem_u32(sm.b[st]);
-          for (int j = 0; j < u.rp / 16; ++j) {
-            const uint64_t ad = sdesc(va + (j >> 2) * (BM * 128) + (j & 3) * 32, 16, 1024);
-            const uint64_t bd = sdesc(ba + j * 2 * kAtomBytes, kAtomBytes, kAtomBytes);
-            mma_bf16(tmem + acc * BN, ad, bd, idesc, j ? 1u : 0u);
+        const uint32_t idesc = idesc_bf16(BM, u.rp, false);
+        for (int s = 0; s < u.nst; ++s, ++seq) {
+          const int st = seq % NS;
+          const int nch = min(u.kpc, u.nchunks - s * u.kpc);
+          mbar_wait(&sm.full[st], (seq / NS) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t base = smem_u32(sm.ring[st]);
+            for (int i = 0; i < nch; ++i) {
+              const uint32_t xa = base + i * u.xb;
+              for (int j = 0; j < u.jps; ++j) {
+                const uint32_t aa = base + u.kpc * u.xb + (i * u.jps + j) * u.bstride;
+                const uint32_t d = tmem + ab * TM_SH + j * u.rp;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_bf16(d, sdesc(xa + kk * 32, 16, 1024), sdesc(aa + kk * 32, 16, kAtomBytes), idesc,
+                           (s | i | kk) ? 1u : 0u);
+              }
+            }
+            mma_commit(&sm.empty[st]);
+            if (s == u.nst - 1) mma_commit(&sm.tfull_sh[ab]);
           }
-          mma_commit(&sm.empty[st]);
-          mma_commit(&sm.tfull[acc]);
-          if (c == nsub - 1) mma_commit(&sm.vempty[vb]);
+          __syncwarp();
         }
-        __syncwarp();
+        ++nsh;
+      } else {
+        const int vb = nex & 1;
+        mbar_wait(&sm.vfull[vb], (nex >> 1) & 1);
+        tc_fence_after();
+        const uint32_t va = smem_u32(sm.vbuf[vb]);
+        for (int s = 0; s < u.nst; ++s, ++seq) {
+          const int st = seq % NS;
+          const int ng = min(u.kpc, u.ngrp - s * u.kpc);
+          mbar_wait(&sm.full[st], (seq / NS) & 1);
+          tc_fence_after();
+          const uint32_t base = smem_u32(sm.ring[st]);
+          for (int g = 0; g < ng; ++g, ++ngrp) {
+            const int acc = ngrp & 1;
+            if (ngrp >= 2) mbar_wait(&sm.tempty_ex[acc], ((ngrp >> 1) - 1) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+              const uint32_t ba = base + g * u.bstride;
+              for (int kk = 0; kk < u.rp / 16; ++kk) {
+                const uint64_t ad = sdesc(va + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
+                const uint64_t bd = sdesc(ba + kk * 2 * kAtomBytes, kAtomBytes, kAtomBytes);
+                mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, kk ? 1u : 0u);
+              }
+              mma_commit(&sm.tfull_ex[acc]);
+            }
+            __syncwarp();
+          }
+          if (lane == 0) {
+            mma_commit(&sm.empty[st]);
+            if (s == u.nst - 1) mma_commit(&sm.vempty[vb]);
+          }
+          __syncwarp();
+        }
+        ++nex;
       }
     }
   } else {
-    // ---------------- warps 0-3: build V (bf16, swizzled), then y += D2 per group
+    // ---------------------------------------------------------------- epilogue warps 0-3
     const int r = warp * 32 + lane;  // tile row == TMEM lane
-    int seq = 0, gi = 0, ui = 0;
-    for (int uu = blockIdx.x; uu < n_units; uu += gridDim.x, ++ui) {
-      const int job = uu / (n_tiles * nq), rem = uu % (n_tiles * nq);
-      const Unit u = make_unit(p, sm.tl, job, rem / nq);
-      const int n0 = (rem % nq) * ncols_unit;
-      const int nsub = min(NSUB, (p.h_out - n0) / BN);
-      const int vb = ui & 1;
-      const bool valid = r < u.m;
-      const int pos = u.row0 + min(r, u.m - 1);
-      const int row = p.perm ? __ldg(p.perm + pos) : pos;
-      if (ui >= 2) mbar_wait(&sm.vempty[vb], ((ui >> 1) - 1) & 1);
-      {
-        const float* vsrc = p.vin + job * p.v_job_stride + (long long)pos * p.ld;
-        const uint32_t vbase = smem_u32(sm.v[vb]);
-        for (int cj = 0; cj < u.rp / 8; ++cj) {
-          float f[8];
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    int seq = 0, nsh = 0, ngrp = 0;
+    for (int k = 0;; ++k) {
+      const int q = k % UQ;
+      mbar_wait(&sm.ufull[q], (k / UQ) & 1);
+      const int u_id = sm.uslot[q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.uempty[q]);
+      if (u_id < 0) break;
+      const Unit u = make_unit(p, tl, u_id);
+      const int pos = u.pos0 + min(r, u.m - 1);
+      if (u.kind == 3) {
+        // ---- MODE_EXPAND phase 1: caller's v rows -> V image
+        if (r < u.mp) {
+          const int nv = r < u.m ? min(u.rank, p.v_stride) : 0;
+          const float* src = p.v_in + (long long)pos * p.v_stride;
+          for (int c0 = 0; c0 < u.rp; c0 += 32) {
+            float v[32];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) f[i] = 0.f;
-          if (valid && cj * 8 < u.rank) {
-            for (int kq = 0; kq < ks; ++kq) {
-              const float4 lo = *reinterpret_cast<const float4*>(vsrc + kq * p.v_ks_stride + cj * 8);
-              const float4 hi = *reinterpret_cast<const float4*>(vsrc + kq * p.v_ks_stride + cj * 8 + 4);
-              f[0] += lo.x; f[1] += lo.y; f[2] += lo.z; f[3] += lo.w;
-              f[4] += hi.x; f[5] += hi.y; f[6] += hi.z; f[7] += hi.w;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (cj * 8 + i >= u.rank) f[i] = 0.f;
+            for (int i = 0; i < 32; ++i) v[i] = c0 + i < nv ? src[c0 + i] : 0.f;
+            write_v_chunk(vimg_of(p, 0, u.tile), u, r, c0, v, nv);
           }
-          const uint4 w = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                                     pack_bf16x2(f[6], f[7]));
-          sts128(vbase + (cj >> 3) * (BM * 128) + swz(r, cj & 7), w);
         }
+        publish_tile(p, u.tile, r);
+        continue;
       }
-      fence_proxy_async_shared();
-      mbar_arrive(&sm.vfull[vb]);
-      char* yrow = p.jobs[job].y + (long long)row * p.h_out * 2;
-      for (int c = 0; c < nsub; ++c, ++seq, ++gi) {
-        const int st = seq % S2, acc = gi & 1;
-        const int col0 = n0 + c * BN;
-        mbar_wait(&sm.tfull[acc], (gi >> 1) & 1);
+      if (u.kind == 1) {
+        // ---- shrink: release the unit's stages, then drain the accumulators
+        for (int s = 0; s < u.nst; ++s, ++seq) {
+          const int st = seq % NS;
+          mbar_wait(&sm.full[st], (seq / NS) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[st]);
+        }
+        const int ab = nsh & 1;
+        mbar_wait(&sm.tfull_sh[ab], (nsh >> 1) & 1);
         tc_fence_after();
-        float d0[32], d1[32];
-        const uint32_t ta = tmem + acc * BN + ((uint32_t)(warp * 32) << 16);
-        tmem_ld32(ta, d0);
-        tmem_ld32(ta + 32, d1);
-        tc_fence_before();
-        mbar_arrive(&sm.tempty[acc]);
-        mbar_wait(&sm.full[st], (seq / S2) & 1);  // the y tile of this group has landed
-        uint4 yv[8];
+        ++nsh;
+        const bool direct = tl.ks == 1 && u.jps == p.n_jobs;  // this unit alone makes the tile's V
+        for (int j = 0; j < u.jps; ++j) {
+          const int job = u.job0 + j;
+          for (int c0 = 0; c0 < u.rank; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + ab * TM_SH + j * u.rp + c0 + lane_off, v);
+            if (p.mode == MODE_SHRINK) {
+              if (r < u.m) {
+                const int nv = min(u.rank, p.v_stride);
+                float* dst = p.v_out + (long long)pos * p.v_stride;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) yv[i] = lds128(sm.y[st] + swz(r, i));
-        mbar_arrive(&sm.empty[st]);
-        if (valid) {
+                for (int i = 0; i < 32; ++i)
+                  if (c0 + i < nv) dst[c0 + i] = v[i];
+              }
+            } else if (direct) {
+              if (r < u.mp) write_v_chunk(vimg_of(p, job, u.tile), u, r, c0, v, r < u.m ? u.rank : 0);
+            } else if (r < u.m) {
+              float* dst = p.part + job * p.part_job + u.kq * p.part_ks + (long long)pos * MAXR + c0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float* d = i < 4 ? d0 + i * 8 : d1 + (i - 4) * 8;
-            float f[8];
-            Elem<__nv_bfloat16>::unpack(yv[i], f);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] += d[e];
-            *reinterpret_cast<uint4*>(yrow + (col0 + i * 8) * 2) = Elem<__nv_bfloat16>::pack(f);
+              for (int i = 0; i < 32; i += 4)
+                if (c0 + i < u.rank) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty_sh[ab]);
+        if (p.mode == MODE_SHRINK) continue;
+        if (direct) {
+          publish_tile(p, u.tile, r);
+          continue;
+        }
+        // split-K / job-group arrival: the last unit of the tile reduces and publishes
+        named_bar_sync(BAR_EPI, 128);
+        if (r == 0) {
+          __threadfence();
+          const int units = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
+          sm.last = atomicAdd(p.tile_cnt + u.tile, 1) == units - 1;
+          __threadfence();
+        }
+        named_bar_sync(BAR_EPI, 128);
+        if (sm.last) {
+          for (int job = 0; job < p.n_jobs; ++job) {
+            if (r >= u.mp) continue;
+            for (int c0 = 0; c0 < u.rp; c0 += 32) {
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              if (r < u.m) {
+                for (int kq = 0; kq < tl.ks; ++kq) {
+                  const float* src = p.part + job * p.part_job + kq * p.part_ks + (long long)pos * MAXR + c0;
+#pragma unroll
+                  for (int i = 0; i < 32; i += 4) {
+                    if (c0 + i < u.rank) {
+                      const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
+                      v[i] += f.x; v[i + 1] += f.y; v[i + 2] += f.z; v[i + 3] += f.w;
+                    }
+                  }
+                }
+              }
+              write_v_chunk(vimg_of(p, job, u.tile), u, r, c0, v, r < u.m ? u.rank : 0);
+            }
+          }
+          publish_tile(p, u.tile, r);
+        }
+        continue;
+      }
+      // ---- expand: y rows += D2 per 64-column group
+      char* yrow = p.jobs[u.job].y + (long long)(p.perm ? __ldg(p.perm + pos) : pos) * p.h_out * 2;
+      const bool valid = r < u.m;
+      for (int s = 0; s < u.nst; ++s, ++seq) {
+        const int st = seq % NS;
+        const int ng = min(u.kpc, u.ngrp - s * u.kpc);
+        mbar_wait(&sm.full[st], (seq / NS) & 1);  // the y rows of this stage have landed
+        const unsigned char* ybase = sm.ring[st] + u.kpc * u.bstride;
+        for (int g = 0; g < ng; ++g, ++ngrp) {
+          const int acc = ngrp & 1;
+          mbar_wait(&sm.tfull_ex[acc], (ngrp >> 1) & 1);
+          tc_fence_after();
+          float d0[32], d1[32];
+          const uint32_t ta = tmem + TM_EX + acc * 64 + lane_off;
+          tmem_ld32(ta, d0);
+          tmem_ld32(ta + 32, d1);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tempty_ex[acc]);
+          if (valid) {
+            const unsigned char* yg = ybase + g * u.xb;
+            const int col0 = u.col0 + (s * u.kpc + g) * 64;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float* d = i < 4 ? d0 + i * 8 : d1 + (i - 4) * 8;
+              float f[8];
+              Elem<__nv_bfloat16>::unpack(lds128(yg + swz(r, i)), f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] += d[e];
+              *reinterpret_cast<uint4*>(yrow + (col0 + i * 8) * 2) = Elem<__nv_bfloat16>::pack(f);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[st]);
       }
     }
   }
+  // the last CTA re-arms this parity's counters
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc<P2_TMEM>(tmem);
+    tmem_dealloc(tmem);
+  }
+  if (tid == 0) {
+    __threadfence();
+    sm.last = atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (sm.last) {
+    for (int i = tid; i < MAX_TILES; i += NTHREADS) p.tile_cnt[i] = 0;
+    if (tid == 0) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+    }
+    __threadfence();
   }
 }
 
@@ -630,8 +846,8 @@ int encode_act_map(CUtensorMap* m, const void* base, int rows, int cols, int box
 }
 }  // namespace
 
-// Launch P1 (unless mode == expand-only) and P2 (unless mode == shrink-only) for the
-// prefill segments of this apply.  mode: 0 fused, 1 shrink (v_out), 2 expand (v_in).
+// Launch the fused tcgen05 kernel for the prefill segments of this apply.
+// mode: 0 fused, 1 shrink only (v_out, TP), 2 expand only (v_in, TP).
 int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
                    void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
                    const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out,
@@ -639,10 +855,10 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   using namespace prefill;
   static bool attr_set = false;
   if (!attr_set) {
-    CHAM_CUDA(cudaFuncSetAttribute(shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P1Shared)));
-    CHAM_CUDA(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(P2Shared)));
+    CHAM_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Shared)));
     attr_set = true;
   }
+  if (mode != MODE_FUSED && n_jobs != 1) return fail(CHAM_ERR_INVALID, "prefill shrink/expand take one projection");
   Params prm{};
   prm.base = pool->base;
   prm.page_bytes = (long long)pool->page_bytes;
@@ -650,6 +866,10 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   prm.h_in = pool->h_in[projs[0]];
   prm.h_out = pool->h_out[projs[0]];
   prm.n_jobs = n_jobs;
+  prm.mode = mode;
+  prm.x_shared = 1;
+  for (int j = 1; j < n_jobs; ++j)
+    if (xs[j] != xs[0]) prm.x_shared = 0;
   for (int j = 0; j < n_jobs; ++j) {
     const int lp = layer * pool->n_proj + projs[j];
     prm.jobs[j].x = static_cast<const char*>(xs[j]);
@@ -664,41 +884,42 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   prm.n_seg = n_seg;
   prm.n_seg_dev = n_seg_dev;
   prm.thr = prefill_route_thr(pool);
-  prm.grid1 = pool->sm_count;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (mode == 0) {
-    prm.split_ok = 1;
-    prm.ld = MAXR;
-    prm.v_ks_stride = (long long)pool->max_tokens * MAXR;
-    prm.v_job_stride = prm.v_ks_stride * kPrefillMaxSplit;
-    prm.vout = pool->d_pws;
-    prm.vin = pool->d_pws;
-  } else {
-    prm.split_ok = 0;
-    prm.ld = v_stride;
-    prm.v_ks_stride = 0;
-    prm.v_job_stride = 0;
-    prm.vout = v_out;
-    prm.vin = v_in;
-  }
-  if (mode != 2) {
-    for (int j = 0; j < n_jobs; ++j) {
-      int rc = encode_act_map(&prm.maps[j].tile, xs[j], n_tokens, prm.h_in, BM);
-      if (!rc) rc = encode_act_map(&prm.maps[j].row, xs[j], n_tokens, prm.h_in, 1);
-      if (rc) return rc;
+  prm.epoch = ++pool->prefill_epoch;
+  int* pc = pool->d_pctr + (prm.epoch & 1) * (kPrefillCtrSet);
+  prm.ctr = pc;
+  prm.tile_cnt = pc + 4;
+  prm.vready = pool->d_pctr + 2 * kPrefillCtrSet;
+  prm.err = pool->d_ctr + 2;
+  prm.part = pool->d_pws;
+  prm.part_ks = (long long)pool->max_tokens * MAXR;
+  prm.part_job = prm.part_ks * kPrefillMaxSplit;
+  prm.vimg = pool->d_pvimg;
+  prm.v_out = v_out;
+  prm.v_in = v_in;
+  prm.v_stride = v_stride;
+  for (int j = 0; j < n_jobs; ++j) {
+    int rc = CHAM_OK;
+    if (mode != MODE_EXPAND) {
+      rc = encode_act_map(&prm.maps[j].x32, xs[j], n_tokens, prm.h_in, 32);
+      if (!rc) rc = encode_act_map(&prm.maps[j].x1, xs[j], n_tokens, prm.h_in, 1);
     }
-    shrink_kernel<<<pool->sm_count, NTHREADS, sizeof(P1Shared), s>>>(prm);
-    CHAM_CUDA(cudaGetLastError());
-  }
-  if (mode != 1) {
-    for (int j = 0; j < n_jobs; ++j) {
-      int rc = encode_act_map(&prm.maps[j].tile, ys[j], n_tokens, prm.h_out, BM);
-      if (!rc) rc = encode_act_map(&prm.maps[j].row, ys[j], n_tokens, prm.h_out, 1);
-      if (rc) return rc;
+    if (!rc && mode != MODE_SHRINK) {
+      rc = encode_act_map(&prm.maps[j].y32, ys[j], n_tokens, prm.h_out, 32);
+      if (!rc) rc = encode_act_map(&prm.maps[j].y1, ys[j], n_tokens, prm.h_out, 1);
     }
-    expand_kernel<<<pool->sm_count, NTHREADS, sizeof(P2Shared), s>>>(prm);
-    CHAM_CUDA(cudaGetLastError());
+    if (rc) return rc;
   }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pool->sm_count);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = sizeof(Shared);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CHAM_CUDA(cudaLaunchKernelEx(&cfg, fused_kernel, prm));
   return CHAM_OK;
 }
 
