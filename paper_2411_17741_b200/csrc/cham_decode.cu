@@ -67,9 +67,15 @@ __host__ __device__ constexpr int tier_pitch(int t) {  // page pitch in a stage 
 #ifndef CHAM_TIERS
 #define CHAM_TIERS 0  // 1: page-count tiers (A/B on C2: 98.1k vs 110.3k tok/s without)
 #endif
-__host__ __device__ constexpr int tier_of_np(int np) {
-  return CHAM_TIERS == 0 ? 0 : np <= 4 ? 0 : np <= 8 ? 1 : 2;
+__host__ __device__ constexpr int tier_of_np(int np) {  // CHAM_TIERS: highest tier used
+  return CHAM_TIERS == 0 ? 0 : np <= 4 ? 0 : (np <= 8 || CHAM_TIERS == 1) ? 1 : 2;
 }
+#ifndef CHAM_EX_DEPTH
+#define CHAM_EX_DEPTH 1  // expand dispatch look-ahead (A/B on C2: 1 -> 114.2k, 2 -> 110.2k tok/s)
+#endif
+#ifndef CHAM_SH_DEPTH
+#define CHAM_SH_DEPTH 1  // shrink dispatch look-ahead (A/B on C2: 1 -> 118.5k, 2 -> 117.2k, 3 -> 114.0k)
+#endif
 constexpr int K2_B = 2 * tier_pitch(0);
 static_assert(4 * tier_pitch(1) <= K2_B && 8 * tier_pitch(2) <= K2_B, "stage layout");
 constexpr int K2_Y = K2_B;
@@ -747,7 +753,7 @@ __device__ __forceinline__ int produce_shrink(const Params& p, Shared& sm, int s
   const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
   const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page of the tile
   UnitQueue uq;
-  uq.init(p.ctr, total, 3, lane, &sm.unit_mailbox);
+  uq.init(p.ctr, total, CHAM_SH_DEPTH, lane, &sm.unit_mailbox);
   int unit = uq.next(lane);
   int4 da = make_int4(0, 0, 0, 0), db = da;
   if (unit >= 0) ldg_desc(desc + unit % US, da, db);
@@ -839,7 +845,7 @@ __device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int s
     return decode_unit(u, t, jc);
   };
   UnitQueue uq;
-  uq.init(p.ctr + 4, total, 2, lane, &sm.unit_mailbox);
+  uq.init(p.ctr + 4, total, CHAM_EX_DEPTH, lane, &sm.unit_mailbox);
   // tile-ready counter of a unit, loaded without blocking (relaxed) when the unit is claimed
   auto peek_ready = [&](int u) {
     int t, jc;

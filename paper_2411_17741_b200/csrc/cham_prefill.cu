@@ -92,6 +92,8 @@ struct alignas(64) Params {
   float* v_out;            // MODE_SHRINK: v [position][v_stride]
   const float* v_in;       // MODE_EXPAND: v [position][v_stride]
   int v_stride;
+  unsigned long long* trace;  // debug timeline [cta][unit k][8] (null = off)
+  int trace_cap;
 };
 
 // ------------------------------------------------------------------ PTX wrappers (tcgen05)
@@ -151,11 +153,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// 2-D TMA tensor store smem -> global (bulk async-group of the issuing thread)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {  // 16-byte chunk of a 128-byte row
   return (uint32_t)(row * 128 + (((chunk ^ row) & 7) << 4));
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// debug timeline: field 0 loader claim, 1 loader issued, 2 MMA start, 3 MMA issued,
+// 4 epilogue start, 5 epilogue end, 6 unit id, 7 kind
+__device__ __forceinline__ void trace_put(const Params& p, int k, int field, unsigned long long v) {
+  if (p.trace && k < p.trace_cap) p.trace[((long long)blockIdx.x * p.trace_cap + k) * 8 + field] = v;
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -326,10 +347,34 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
 
 // Token rows of one 32-row block of a tile as seen by a loader lane: the block is contiguous
 // when its rows are consecutive tokens (one TMA box), else each lane loads its own row.
-__device__ __forceinline__ int block_row(const Params& p, const Unit& u, int blk, int lane, bool& contig) {
+// Per-unit global reads of the loader (token rows of the tile, adapter page ids), issued one
+// unit ahead so their L2 round trip overlaps the current unit's copies.
+struct Prefetch {
+  int rows[4];  // lane l: row of tile position 32 b + l (clamped to the last row)
+  int page;     // lane l < np: pool page l of the adapter
+};
+__device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileList& tl, int u_id, int lane) {
+  Prefetch f;
+  f.page = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) f.rows[b] = 0;
+  if (u_id < 0 || u_id >= tl.u_total || (u_id < tl.u1 && p.mode == MODE_EXPAND)) return f;
+  const Tile& t = tl.t[u_id < tl.u1 ? tile_of_unit(tl, u_id)
+                                    : (u_id - tl.u1) / (p.n_jobs * ((p.h_out + CW - 1) / CW))];
+  const int np = (t.rank + 7) / 8;
+  if (lane < np) f.page = __ldg(p.slot_pages + t.slot * kMaxPagesPerSlot + lane);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int pos = t.pos0 + min(b * 32 + lane, t.m - 1);
+    if (b * 32 < t.m) f.rows[b] = p.perm ? __ldg(p.perm + pos) : pos;
+  }
+  return f;
+}
+// Token row of block `blk` for this lane; `contig` = the block's rows are consecutive tokens
+// (one TMA box), else each lane moves its own row.
+__device__ __forceinline__ int block_row(const Prefetch& f, const Unit& u, int blk, int lane, bool& contig) {
   const int r = blk * 32 + lane;
-  const int pos = u.pos0 + min(r, u.m - 1);
-  const int row = p.perm ? __ldg(p.perm + pos) : pos;
+  const int row = f.rows[blk];
   const int first = __shfl_sync(0xffffffffu, row, 0);
   contig = __all_sync(0xffffffffu, r >= u.m || row == first + lane);
   return row;
@@ -445,8 +490,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       return v;
     };
     int flag = peek_flag(next);
+    Prefetch pf = prefetch_unit(p, tl, next, lane);
     int seq = 0, nex = 0;
     for (int k = 0;; ++k) {
+      if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 1, gtimer());
       const int u_id = __shfl_sync(0xffffffffu, next < tl.u_total ? next : -1, 0);
       // publish the unit id to the MMA and epilogue warps
       const int q = k % UQ;
@@ -460,16 +507,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       if (lane == 0 && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
       const int cur_flag = flag;
       flag = peek_flag(next);
+      const Prefetch cf = pf;
+      pf = prefetch_unit(p, tl, next, lane);
       const Unit u = make_unit(p, tl, u_id);
+      if (lane == 0 && p.trace) {
+        trace_put(p, k, 0, gtimer());
+        trace_put(p, k, 6, u_id);
+        trace_put(p, k, 7, u.kind);
+      }
       if (u.kind == 3) continue;
-      const int my_page = lane < u.np ? __ldg(p.slot_pages + u.slot * kMaxPagesPerSlot + lane) : 0;
+      const int my_page = cf.page;
       if (u.kind == 1) {
         // ---- shrink: x chunks of the tile + A^T atoms of every job of the group
         const int nblk = (u.m + 31) / 32;
         bool contig[4];
         int rows[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(p, u, b, lane, contig[b]) : 0;
+        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(cf, u, b, lane, contig[b]) : 0;
         const int kc0 = u.kq * u.nchunks;
         const int n_cp = u.jps * u.np;  // A copies per chunk
         for (int s = 0; s < u.nst; ++s, ++seq) {
@@ -526,7 +580,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         bool contig[4];
         int rows[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(p, u, b, lane, contig[b]) : 0;
+        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(cf, u, b, lane, contig[b]) : 0;
         const bool pad = (u.rp / 8) > u.np;
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
@@ -576,6 +630,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     int seq = 0, nsh = 0, nex = 0, ngrp = 0;
     const uint32_t idesc_ex = idesc_bf16(BM, 64, true);
     for (int k = 0;; ++k) {
+      if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 3, gtimer());
       const int q = k % UQ;
       mbar_wait(&sm.ufull[q], (k / UQ) & 1);
       const int u_id = sm.uslot[q];
@@ -583,6 +638,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
       if (u_id < 0) break;
       const Unit u = make_unit(p, tl, u_id);
+      if (lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
       if (u.kind == 3) continue;
       if (u.kind == 1) {
         const int ab = nsh & 1;
@@ -654,6 +710,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     int seq = 0, nsh = 0, ngrp = 0;
     for (int k = 0;; ++k) {
+      if (k > 0 && r == 0 && p.trace) trace_put(p, k - 1, 5, gtimer());
       const int q = k % UQ;
       mbar_wait(&sm.ufull[q], (k / UQ) & 1);
       const int u_id = sm.uslot[q];
@@ -661,6 +718,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
       if (u_id < 0) break;
       const Unit u = make_unit(p, tl, u_id);
+      if (r == 0 && p.trace) trace_put(p, k, 4, gtimer());
       const int pos = u.pos0 + min(r, u.m - 1);
       if (u.kind == 3) {
         // ---- MODE_EXPAND phase 1: caller's v rows -> V image
@@ -756,9 +814,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         }
         continue;
       }
-      // ---- expand: y rows += D2 per 64-column group
-      char* yrow = p.jobs[u.job].y + (long long)(p.perm ? __ldg(p.perm + pos) : pos) * p.h_out * 2;
+      // ---- expand: y rows += D2 per 64-column group.  Each thread adds its row in place in
+      // the staged y tile; then the warp stores its 32 rows coalesced (8 lanes per 128-byte
+      // row, 4 rows per instruction) instead of 32 rows x 16 B per instruction.
+      const int yrow_idx = p.perm ? __ldg(p.perm + pos) : pos;
       const bool valid = r < u.m;
+      char* const ybase_g = p.jobs[u.job].y;
       for (int s = 0; s < u.nst; ++s, ++seq) {
         const int st = seq % NS;
         const int ng = min(u.kpc, u.ngrp - s * u.kpc);
@@ -775,9 +836,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.tempty_ex[acc]);
+          const int col0 = u.col0 + (s * u.kpc + g) * 64;
+          unsigned char* yg = const_cast<unsigned char*>(ybase) + g * u.xb;
           if (valid) {
-            const unsigned char* yg = ybase + g * u.xb;
-            const int col0 = u.col0 + (s * u.kpc + g) * 64;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float* d = i < 4 ? d0 + i * 8 : d1 + (i - 4) * 8;
@@ -785,7 +846,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
               Elem<__nv_bfloat16>::unpack(lds128(yg + swz(r, i)), f);
 #pragma unroll
               for (int e = 0; e < 8; ++e) f[e] += d[e];
-              *reinterpret_cast<uint4*>(yrow + (col0 + i * 8) * 2) = Elem<__nv_bfloat16>::pack(f);
+              const uint4 w = Elem<__nv_bfloat16>::pack(f);
+              asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(yg + swz(r, i))), "r"(w.x), "r"(w.y),
+                           "r"(w.z), "r"(w.w)
+                           : "memory");
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + (lane >> 3);  // row of this warp's block
+            const int c = lane & 7;              // 16-byte chunk of the row
+            const int grow = __shfl_sync(0xffffffffu, yrow_idx, rr);
+            if (warp * 32 + rr < u.m) {
+              const uint4 w = lds128(yg + swz(warp * 32 + rr, c));
+              *reinterpret_cast<uint4*>(ybase_g + ((long long)grow * p.h_out + col0 + c * 8) * 2) = w;
             }
           }
         }
@@ -897,6 +972,10 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   prm.v_out = v_out;
   prm.v_in = v_in;
   prm.v_stride = v_stride;
+  if (pool->d_trace) {  // second half of the debug buffer (the first is the decode kernel's)
+    prm.trace = pool->d_trace + (size_t)pool->sm_count * pool->trace_cap * 8;
+    prm.trace_cap = pool->trace_cap;
+  }
   for (int j = 0; j < n_jobs; ++j) {
     int rc = CHAM_OK;
     if (mode != MODE_EXPAND) {
