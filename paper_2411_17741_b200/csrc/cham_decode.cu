@@ -41,15 +41,22 @@ namespace decode {
 #define CHAM_EXP_NOCOMPUTE 0  // experiment builds only: consumers skip the math (data-movement ceiling)
 #endif
 constexpr bool kNoCompute = CHAM_EXP_NOCOMPUTE != 0;
-#ifndef CHAM_SHRINK_LPT
-#define CHAM_SHRINK_LPT 1  // shrink units in LPT order (else segment order)
-#endif
-constexpr bool kShrinkLpt = CHAM_SHRINK_LPT != 0;
+
 constexpr int TG = 4;                        // tokens per tile
-constexpr int NSTAGE = 4;
-constexpr int A_CHUNK = 32768;               // K1: adapter bytes per stage (8 rows x 4 KiB)
+#ifndef CHAM_NSTAGE
+#define CHAM_NSTAGE 4
+#endif
+#ifndef CHAM_ACHUNK
+#define CHAM_ACHUNK 32768
+#endif
+#ifndef CHAM_EXPG
+#define CHAM_EXPG 2
+#endif
+constexpr int NSTAGE = CHAM_NSTAGE;          // ring depth
+constexpr int A_CHUNK = CHAM_ACHUNK;         // K1: adapter bytes per stage (8 rows x A_CHUNK/8)
 constexpr int X_ROW = A_CHUNK / kRowsPerPage;  // K1: x bytes per token per stage (k-chunk)
-static_assert(X_ROW == kActRowBytes, "pool workspace geometry");
+constexpr int EX_PAGES = CHAM_EXPG;          // K2: adapter pages per stage (1 or 2)
+static_assert(X_ROW <= kActRowBytes && (EX_PAGES == 1 || EX_PAGES == 2), "stage geometry");
 constexpr int K1_STAGE = A_CHUNK + TG * X_ROW;
 // K2 geometry tiers, chosen by the adapter's page count np so that every expand unit is at
 // most two 32 KiB stages (uniform units keep the dynamic dispatch balanced to the end —
@@ -76,8 +83,8 @@ __host__ __device__ constexpr int tier_of_np(int np) {  // CHAM_TIERS: highest t
 #ifndef CHAM_SH_DEPTH
 #define CHAM_SH_DEPTH 1  // shrink dispatch look-ahead (A/B on C2: 1 -> 118.5k, 2 -> 117.2k, 3 -> 114.0k)
 #endif
-constexpr int K2_B = 2 * tier_pitch(0);
-static_assert(4 * tier_pitch(1) <= K2_B && 8 * tier_pitch(2) <= K2_B, "stage layout");
+constexpr int K2_B = (CHAM_TIERS ? 2 : EX_PAGES) * tier_pitch(0);
+static_assert(CHAM_TIERS == 0 || (4 * tier_pitch(1) <= K2_B && 8 * tier_pitch(2) <= K2_B), "stage layout");
 constexpr int K2_Y = K2_B;
 constexpr int K2_V = K2_Y + TG * NCB_SMALL;
 constexpr int K2_STAGE = K2_V + 8 * TG * kRowsPerPage * 4;  // v slice [page][token][8 rows]
@@ -165,8 +172,9 @@ struct alignas(16) Plan {
   int scan[NTHREADS / 32][4];
   int totals[6];  // K1 units/job, K2 tiles/job, tokens, pages, v floats/job, segments with work
   int n_seg;
-  int tier_tiles[NTIER];     // leading LPT tiles of tier >= t (tier_tiles[0] = all tiles)
-  int tier_seg[NTIER];       // leading LPT segments of tier >= t
+  int sh_lpt[PLAN_SEGS + 1];  // K1 unit prefix by LPT position
+  int cls_pos[kMaxPagesPerSlot + 2];  // LPT positions where the page-count classes start
+  int n_cls;
   int order_pos[PLAN_SEGS];  // segment -> position in the LPT order
   long long desc_cap;        // descriptor capacity (entries) after the header
 };
@@ -188,6 +196,18 @@ __host__ __device__ inline long long plan_desc_capacity(int max_tokens) {
   return (long long)max_tokens * (kMaxPagesPerSlot + 1);
 }
 
+constexpr int MAX_BLOCKS = 2 * (kMaxPagesPerSlot + 1);
+#ifndef CHAM_STAGGER
+#define CHAM_STAGGER 0  // 1: S(0) S(1) E(0) S(2) E(1) ... (A/B on C2: 103.5k vs 118.5k tok/s for S... E...)
+#endif
+constexpr bool kStagger = CHAM_STAGGER != 0;
+struct Schedule {
+  int n;
+  int start[MAX_BLOCKS + 1];  // unit prefix
+  int kind[MAX_BLOCKS];       // KIND_SHRINK / KIND_EXPAND
+  int a[MAX_BLOCKS], e[MAX_BLOCKS];  // LPT positions [a, e) of the class
+};
+
 constexpr int STAGE_BYTES = K1_STAGE > K2_STAGE ? K1_STAGE : K2_STAGE;
 constexpr int SCRATCH_BYTES = TG * kMaxRank * 4;  // K2 v rows; K1 uses the first 1 KiB
 struct Shared {
@@ -201,8 +221,10 @@ struct Shared {
   int* pub_slot[PQ];
   uint64_t pub_full[PQ], pub_empty[PQ];
   int unit_mailbox;
+  Schedule sched;
   Plan plan;
 };
+static_assert(sizeof(Shared) <= 227 * 1024, "decode kernel shared memory exceeds the 227 KiB per-CTA limit");
 using K1Shared = Shared;
 using K2Shared = Shared;
 
@@ -330,16 +352,15 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
   if (pl.totals[2] > p.max_tokens) return false;
   // LPT order for K2: bucket offsets by decreasing page count, then scatter segments
   if (tid == 0) {
-    int acc = 0;
-    for (int t = 0; t < NTIER; ++t) pl.tier_seg[t] = 0;
+    int acc = 0, ncls = 0;
     for (int np = kMaxPagesPerSlot; np >= 1; --np) {
       const int c = pl.bucket[np];
+      if (c > 0) pl.cls_pos[ncls++] = acc;  // one class per page count present
       pl.bucket[np] = acc;
       acc += c;
-      for (int t = 1; t < NTIER; ++t)
-        if (tier_of_np(np) >= t) pl.tier_seg[t] = acc;  // higher tiers lead the order
     }
-    pl.tier_seg[0] = acc;
+    pl.cls_pos[ncls] = acc;
+    pl.n_cls = ncls;
     pl.totals[5] = acc;  // segments with work
   }
   __syncthreads();
@@ -389,15 +410,16 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
       }
       if (i < nw) {
         pl.ex_start[i] = carry + inc - u;
-        if (kShrinkLpt) pl.sh_start[s] = carry_sh + inc_sh - ush;
+        pl.sh_lpt[i] = carry_sh + inc_sh - ush;
+        pl.sh_start[s] = carry_sh + inc_sh - ush;
       }
       carry += __shfl_sync(0xffffffffu, inc, 31);
       carry_sh += __shfl_sync(0xffffffffu, inc_sh, 31);
     }
     if (lane == 0) {
       pl.ex_start[nw] = carry;
+      pl.sh_lpt[nw] = carry_sh;
       pl.totals[1] = carry;
-      for (int t = 0; t < NTIER; ++t) pl.tier_tiles[t] = pl.ex_start[pl.tier_seg[t]];
     }
   }
   __syncthreads();
@@ -741,239 +763,266 @@ __device__ __forceinline__ void ldg_desc(const UnitDesc* d, int4& a, int4& b) {
   b = __ldg(q + 1);
 }
 
+// The producer's unit stream.  Segments are grouped into classes of equal page count np,
+// largest first (the LPT order of the plan).  Every class c contributes a block of shrink
+// units S(c) (job, 4-token tile, page) and a block of expand units E(c) (tile, job,
+// 1024-column chunk), dispatched from ONE counter in the order
+//     S(0) S(1) E(0) S(2) E(1) ... S(C-1) E(C-2) E(C-1)
+// so the long expand units of the large-rank tiles start while shrink work is still in
+// flight (instead of after all of it), and each E(c) follows its S(c) by one class: by the
+// time an expand unit is claimed its tile's v rows are (nearly always) published.
+// MODE_SHRINK streams the S blocks only, MODE_EXPAND the E blocks only.
 template <typename T>
-__device__ __forceinline__ int produce_shrink(const Params& p, Shared& sm, int seq, bool& waited) {
+__device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedule& sc) {
+  const int J = p.n_jobs;
+  const int ncc = n_colchunks<T>(p, 0);
+  int n = 0, acc = 0;
+  auto add = [&](int kind, int a, int e) {
+    const int units = kind == KIND_SHRINK ? J * (pl.sh_lpt[e] - pl.sh_lpt[a]) : J * ncc * (pl.ex_start[e] - pl.ex_start[a]);
+    if (units <= 0) return;
+    sc.kind[n] = kind;
+    sc.a[n] = a;
+    sc.e[n] = e;
+    sc.start[n] = acc;
+    acc += units;
+    ++n;
+  };
+  const int C = pl.n_cls;
+  if (kStagger) {
+    for (int c = 0; c < C; ++c) {
+      if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[c], pl.cls_pos[c + 1]);
+      if (mode != MODE_SHRINK && c >= 1) add(KIND_EXPAND, pl.cls_pos[c - 1], pl.cls_pos[c]);
+    }
+    if (mode != MODE_SHRINK && C >= 1) add(KIND_EXPAND, pl.cls_pos[C - 1], pl.cls_pos[C]);
+  } else {
+    if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[0], pl.cls_pos[C]);
+    if (mode != MODE_SHRINK) add(KIND_EXPAND, pl.cls_pos[0], pl.cls_pos[C]);
+  }
+  sc.start[n] = acc;
+  sc.n = n;
+}
+
+// unit -> (block, job, descriptor index, column chunk)
+struct UnitPos {
+  int kind, job, di, cc;
+};
+template <typename T>
+__device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const Schedule& sc, int u) {
+  int b = 0;
+  while (b + 1 < sc.n && sc.start[b + 1] <= u) ++b;
+  const int rel = u - sc.start[b];
+  UnitPos r;
+  r.kind = sc.kind[b];
+  if (r.kind == KIND_SHRINK) {
+    const int span = pl.sh_lpt[sc.e[b]] - pl.sh_lpt[sc.a[b]];
+    r.job = rel / span;
+    r.di = pl.sh_lpt[sc.a[b]] + (rel - r.job * span);
+    r.cc = 0;
+  } else {
+    const int ncc = n_colchunks<T>(p, 0);
+    const int per_tile = p.n_jobs * ncc;
+    r.di = pl.ex_start[sc.a[b]] + rel / per_tile;  // expand tile
+    const int jc = rel % per_tile;
+    r.job = jc / ncc;
+    r.cc = jc - r.job * ncc;
+  }
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq, bool& waited, int job, int4 da,
+                                            int4 db) {
   constexpr int ES = Elem<T>::kBytes;
   const int lane = threadIdx.x & 31;
-  const int US = sm.plan.totals[0];
-  const int total = p.n_jobs * US;
   const int nkc = n_kchunks<T>(p);
   const int natoms = p.h_in * ES / kRowBytes;
-  const UnitDesc* desc = reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan));
   const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
   const uint64_t pol_x = policy_evict_last();   // x rows: re-read by every page of the tile
-  UnitQueue uq;
-  uq.init(p.ctr, total, CHAM_SH_DEPTH, lane, &sm.unit_mailbox);
-  int unit = uq.next(lane);
-  int4 da = make_int4(0, 0, 0, 0), db = da;
-  if (unit >= 0) ldg_desc(desc + unit % US, da, db);
-  while (unit >= 0) {
-    // prefetch the next unit's descriptor while this one streams
-    const int nunit = uq.next(lane);
-    int4 na = da, nb = db;
-    if (nunit >= 0) ldg_desc(desc + nunit % US, na, nb);
-    const int job = unit / US;
-    const int s = da.x, pos0 = da.y;
-    const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff, g = da.z >> 16;
-    const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
-    const Job& jb = p.jobs[job];
-    const char* a_src = p.base + (long long)da.w * p.page_bytes + jb.a_off;
-    for (int kc = 0; kc < nkc; ++kc, ++seq) {
-      const unsigned long long t_it = p.trace ? gtimer() : 0;
-      const int stage = seq % NSTAGE;
-      const int a0 = kc * (A_CHUNK / kAtomBytes);
-      const uint32_t a_bytes = min(A_CHUNK / kAtomBytes, natoms - a0) * kAtomBytes;
-      const uint32_t x_bytes = a_bytes / kRowsPerPage;
-      unsigned char* st = sm.stage[stage];
-      if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
-      const unsigned long long t_ready = p.trace ? gtimer() : 0;
-      __syncwarp();
-      Meta& m = sm.meta[stage];
-      if (lane == 0) {
-        m.kind = KIND_SHRINK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
-        m.g = g; m.kc = kc;
-        mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
-        bulk_g2s(st, a_src + (long long)a0 * kAtomBytes, a_bytes, &sm.full[stage], pol_w);
-      }
-      if (lane < tcount) m.rows[lane] = row;
-      if (!waited) {  // x may be produced by the previous kernel
-        pdl_wait();
-        pdl_launch_dependents();
-        waited = true;
-      }
-      if (lane < tcount)
-        bulk_g2s(st + A_CHUNK + lane * X_ROW, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
-                 &sm.full[stage], pol_x);
-      if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
-      __syncwarp();
+  const int s = da.x, pos0 = da.y;
+  const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff, g = da.z >> 16;
+  const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
+  const Job& jb = p.jobs[job];
+  const char* a_src = p.base + (long long)da.w * p.page_bytes + jb.a_off;
+  for (int kc = 0; kc < nkc; ++kc, ++seq) {
+    const unsigned long long t_it = p.trace ? gtimer() : 0;
+    const int stage = seq % NSTAGE;
+    const int a0 = kc * (A_CHUNK / kAtomBytes);
+    const uint32_t a_bytes = min(A_CHUNK / kAtomBytes, natoms - a0) * kAtomBytes;
+    const uint32_t x_bytes = a_bytes / kRowsPerPage;
+    unsigned char* st = sm.stage[stage];
+    if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+    const unsigned long long t_ready = p.trace ? gtimer() : 0;
+    __syncwarp();
+    Meta& m = sm.meta[stage];
+    if (lane == 0) {
+      m.kind = KIND_SHRINK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+      m.g = g; m.kc = kc;
+      mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
+      bulk_g2s(st, a_src + (long long)a0 * kAtomBytes, a_bytes, &sm.full[stage], pol_w);
     }
-    unit = nunit;
-    da = na;
-    db = nb;
+    if (lane < tcount) m.rows[lane] = row;
+    if (!waited) {  // x may be produced by the previous kernel
+      pdl_wait();
+      pdl_launch_dependents();
+      waited = true;
+    }
+    if (lane < tcount)
+      bulk_g2s(st + A_CHUNK + lane * X_ROW, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
+               &sm.full[stage], pol_x);
+    if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
+    __syncwarp();
   }
   return seq;
 }
 
-// Producer side of phase 2 (expand units).  Unit space: first the tiles with >= 16 pages
-// (512-column units, 4 pages per stage), then the rest (1024-column units, 2 pages per
-// stage); inside each region unit = (tile_lpt * n_jobs + job) * ncc + cc, so the
-// largest-rank tiles of every job go first.  In fused mode the v copies wait for the grid
-// barrier (every CTA finished phase 1); B pages and y rows are prefetched before it.
 template <typename T>
-__device__ __forceinline__ int produce_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused) {
+__device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused, int job,
+                                            int cc, int tile, int4 da, int4 db, int rdy, int unit) {
   constexpr int ES = Elem<T>::kBytes;
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
-  const int J = p.n_jobs;
   const int NTL = pl.totals[1];
-  // unit space: tier 2 tiles, then tier 1, then tier 0 (the LPT order); inside a tier
-  // unit = (tile * n_jobs + job) * ncc + column chunk
-  int ubase[NTIER + 1], ncc[NTIER];
-  ubase[NTIER] = 0;
-#pragma unroll
-  for (int t = NTIER - 1; t >= 0; --t) {
-    ncc[t] = n_colchunks<T>(p, t);
-    const int t_end = t == 0 ? NTL : pl.tier_tiles[t];
-    const int t_beg = t == NTIER - 1 ? 0 : pl.tier_tiles[t + 1];
-    ubase[t] = ubase[t + 1] + (t_end - t_beg) * J * ncc[t];
-  }
-  const int total = ubase[0];
   const bool pages_smem = pl.totals[3] <= PLAN_PAGES;
-  const UnitDesc* desc =
-      reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan)) + pl.totals[0];
   const uint64_t pol_w = policy_evict_first();
-  // unit -> (tier, tile, job * ncc + column chunk)
-  auto decode_unit = [&](int u, int& tier, int& jc) {
-    tier = u < ubase[2] ? 2 : u < ubase[1] ? 1 : 0;
-    const int rel = u - (tier == 2 ? 0 : ubase[tier + 1]);
-    const int tile0 = tier == 2 ? 0 : pl.tier_tiles[tier + 1];
-    jc = rel % (J * ncc[tier]);
-    return tile0 + rel / (J * ncc[tier]);
-  };
-  auto tile_of = [&](int u) {
-    int t, jc;
-    return decode_unit(u, t, jc);
-  };
-  UnitQueue uq;
-  uq.init(p.ctr + 4, total, CHAM_EX_DEPTH, lane, &sm.unit_mailbox);
-  // tile-ready counter of a unit, loaded without blocking (relaxed) when the unit is claimed
-  auto peek_ready = [&](int u) {
-    int t, jc;
-    const int tl = decode_unit(u, t, jc);
-    int v = 0;
-    if (fused && lane == 0) {
-      const int* c = p.tile_ctr + (jc / ncc[t]) * NTL + tl;
-      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+  const int s = da.x, pos0 = da.y;
+  const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff;
+  const int vbase = da.w;
+  const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
+  const int slot = pl.seg_sr[s] >> 9;
+  const int lpg = 1;           // two consumer threads per 16-byte column chunk
+  const int pgs = EX_PAGES;    // one page per stage: the two threads split its rows
+  const int ncb = tier_ncb(0);
+  const int pitch = tier_pitch(0);
+  const int ncol_unit = ncb / ES;
+  const int col0 = cc * ncol_unit;
+  const int ncols = min(ncol_unit, p.h_out - col0);
+  const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
+  const uint32_t y_bytes = ncols * ES;                  // per token
+  const int rpad = np * kRowsPerPage;
+  const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
+  const int nst = ceil_div(np, pgs);
+  const Job& jb = p.jobs[job];
+  for (int k = 0; k < nst; ++k, ++seq) {
+    const unsigned long long t_it = p.trace ? gtimer() : 0;
+    const int stage = seq % NSTAGE;
+    const int pg0 = k * pgs;
+    const int npg = min(pgs, np - pg0);
+    unsigned char* st = sm.stage[stage];
+    // every stage carries its pages' v slice; the last one also the y rows.  With a
+    // caller-provided v (TP) only pages inside v_stride are copied, the rest are zeroed.
+    const int npg_in = p.v_in ? max(0, min(npg, vrow / kRowsPerPage - pg0)) : npg;
+    const uint32_t v_bytes = p.v_in ? npg_in * tcount * kRowsPerPage * 4 : npg * TG * kRowsPerPage * 4;
+    uint32_t bytes = b_bytes * npg + v_bytes;
+    if (k == nst - 1) bytes += y_bytes * tcount;
+    int pgid = 0;
+    if (lane < npg) pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
+    if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+    const unsigned long long t_ready = p.trace ? gtimer() : 0;
+    __syncwarp();
+    if (p.v_in && npg_in < npg) {
+      for (int c2 = lane; c2 < (npg - npg_in) * tcount; c2 += 32) {
+        const int hh = npg_in + c2 / tcount, t = c2 % tcount;
+        float4* z = reinterpret_cast<float4*>(st + K2_V + (hh * TG + t) * kRowsPerPage * 4);
+        z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      fence_proxy_async_shared();  // generic zero stores before later TMA writes to the stage
+      __syncwarp();
     }
-    return v;
+    Meta& m = sm.meta[stage];
+    if (lane == 0) {
+      m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+      m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
+      m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16;
+      mbar_arrive_expect_tx(&sm.full[stage], bytes);
+    }
+    if (lane < tcount) m.rows[lane] = row;
+    // B pages of this stage (weights: independent of phase 1 and of the previous kernel)
+    if (lane < npg) {
+      const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
+      bulk_g2s(st + lane * pitch, src, b_bytes, &sm.full[stage], pol_w);
+    }
+    if (!waited) {  // y may be produced by the previous kernel
+      pdl_wait();
+      pdl_launch_dependents();
+      waited = true;
+    }
+    if (k == nst - 1 && lane < tcount)
+      bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
+    if (fused && k == 0) {
+      // the tile's v rows are complete once all np shrink units of (job, tile) published
+      // (writers: v stores, proxy fence; publisher warp: gpu fence, counter).  The counter
+      // was peeked when the unit was claimed; only a tile still in flight then is polled.
+      if (lane == 0 && rdy < np) {
+        const int* c = p.tile_ctr + job * NTL + tile;
+        while (ld_acquire_gpu(c) < np) __nanosleep(20);
+      }
+      __syncwarp();
+    }
+    if (p.v_in) {
+      // TP: v [position][v_stride] -> stage [page][token][8], one 32-byte copy each
+      for (int c2 = lane; c2 < npg_in * tcount; c2 += 32) {
+        const int hh = c2 / tcount, t = c2 - hh * tcount;
+        const int r0 = (pg0 + hh) * kRowsPerPage;
+        bulk_g2s(st + K2_V + (hh * TG + t) * kRowsPerPage * 4, p.v_in + (long long)(pos0 + t) * p.v_stride + r0,
+                 kRowsPerPage * 4, &sm.full[stage], pol_w);
+      }
+    } else if (lane == 0) {
+      bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase + pg0 * TG * kRowsPerPage, v_bytes, &sm.full[stage],
+               pol_w);
+    }
+    if (lane == 0) {
+      trace_producer(p, seq, t_it, t_ready, 2, bytes);
+      if (p.trace && seq < p.trace_cap) {
+        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 6] = unit;
+        p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 7] = (np << 8) | tcount;
+      }
+    }
+    __syncwarp();
+  }
+  return seq;
+}
+
+template <typename T>
+__device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq, bool& waited, int mode) {
+  const Plan& pl = sm.plan;
+  const int lane = threadIdx.x & 31;
+  const bool fused = mode == MODE_FUSED;
+  Schedule& sc = sm.sched;
+  if (lane == 0) build_schedule<T>(p, pl, mode, sc);
+  __syncwarp();
+  const int total = sc.start[sc.n];
+  const int NTL = pl.totals[1];
+  const UnitDesc* desc = reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan));
+  UnitQueue uq;
+  uq.init(p.ctr, total, CHAM_SH_DEPTH, lane, &sm.unit_mailbox);
+  // descriptor and (expand) tile-ready counter of a unit, fetched one unit ahead (relaxed)
+  auto fetch = [&](int u, UnitPos& up, int4& a, int4& b, int& rdy) {
+    up = locate<T>(p, pl, sc, u);
+    ldg_desc(desc + (up.kind == KIND_SHRINK ? up.di : pl.totals[0] + up.di), a, b);
+    rdy = 0;
+    if (up.kind == KIND_EXPAND && fused && lane == 0) {
+      const int* c = p.tile_ctr + up.job * NTL + up.di;
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(rdy) : "l"(c) : "memory");
+    }
   };
   int unit = uq.next(lane);
+  UnitPos up{};
   int4 da = make_int4(0, 0, 0, 0), db = da;
   int rdy = 0;
-  if (unit >= 0) {
-    ldg_desc(desc + tile_of(unit), da, db);
-    rdy = peek_ready(unit);
-  }
+  if (unit >= 0) fetch(unit, up, da, db, rdy);
   while (unit >= 0) {
     const int nunit = uq.next(lane);
+    UnitPos nup = up;
     int4 na = da, nb = db;
     int nrdy = 0;
-    if (nunit >= 0) {
-      ldg_desc(desc + tile_of(nunit), na, nb);
-      nrdy = peek_ready(nunit);
-    }
-    int tier, jc;
-    const int tile = decode_unit(unit, tier, jc);
-    const int job = jc / ncc[tier];
-    const int cc = jc - job * ncc[tier];
-    const int s = da.x, pos0 = da.y;
-    const int tcount = da.z & 0xff, np = (da.z >> 8) & 0xff;
-    const int vbase = da.w;
-    const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
-    const int slot = pl.seg_sr[s] >> 9;
-    const int lpg = tier + 1;
-    const int pgs = 1 << lpg;
-    const int ncb = tier_ncb(tier);
-    const int pitch = tier_pitch(tier);
-    const int ncol_unit = ncb / ES;
-    const int col0 = cc * ncol_unit;
-    const int ncols = min(ncol_unit, p.h_out - col0);
-    const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
-    const uint32_t y_bytes = ncols * ES;                  // per token
-    const int rpad = np * kRowsPerPage;
-    const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
-    const int nst = ceil_div(np, pgs);
-    const Job& jb = p.jobs[job];
-    for (int k = 0; k < nst; ++k, ++seq) {
-      const unsigned long long t_it = p.trace ? gtimer() : 0;
-      const int stage = seq % NSTAGE;
-      const int pg0 = k * pgs;
-      const int npg = min(pgs, np - pg0);
-      unsigned char* st = sm.stage[stage];
-      // every stage carries its pages' v slice; the last one also the y rows.  With a
-      // caller-provided v (TP) only pages inside v_stride are copied, the rest are zeroed.
-      const int npg_in = p.v_in ? max(0, min(npg, vrow / kRowsPerPage - pg0)) : npg;
-      const uint32_t v_bytes = p.v_in ? npg_in * tcount * kRowsPerPage * 4 : npg * TG * kRowsPerPage * 4;
-      uint32_t bytes = b_bytes * npg + v_bytes;
-      if (k == nst - 1) bytes += y_bytes * tcount;
-      int pgid = 0;
-      if (lane < npg) pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
-      if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
-      const unsigned long long t_ready = p.trace ? gtimer() : 0;
-      __syncwarp();
-      if (p.v_in && npg_in < npg) {
-        for (int c2 = lane; c2 < (npg - npg_in) * tcount; c2 += 32) {
-          const int hh = npg_in + c2 / tcount, t = c2 % tcount;
-          float4* z = reinterpret_cast<float4*>(st + K2_V + (hh * TG + t) * kRowsPerPage * 4);
-          z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-          z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        fence_proxy_async_shared();  // generic zero stores before later TMA writes to the stage
-        __syncwarp();
-      }
-      Meta& m = sm.meta[stage];
-      if (lane == 0) {
-        m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
-        m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
-        m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16;
-        mbar_arrive_expect_tx(&sm.full[stage], bytes);
-      }
-      if (lane < tcount) m.rows[lane] = row;
-      // B pages of this stage (weights: independent of phase 1 and of the previous kernel)
-      if (lane < npg) {
-        const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;
-        bulk_g2s(st + lane * pitch, src, b_bytes, &sm.full[stage], pol_w);
-      }
-      if (!waited) {  // y may be produced by the previous kernel
-        pdl_wait();
-        pdl_launch_dependents();
-        waited = true;
-      }
-      if (k == nst - 1 && lane < tcount)
-        bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage],
-                 pol_w);
-      if (fused && k == 0) {
-        // the tile's v rows are complete once all np shrink units of (job, tile) published
-        // (writers: v stores, proxy fence, gpu fence, counter).  The counter was peeked when
-        // the unit was claimed; only a tile still in flight then is polled here.
-        if (lane == 0 && rdy < np) {
-          const int* c = p.tile_ctr + job * NTL + tile;
-          while (ld_acquire_gpu(c) < np) __nanosleep(20);
-        }
-        __syncwarp();
-      }
-      if (p.v_in) {
-        // TP: v [position][v_stride] -> stage [page][token][8], one 32-byte copy each
-        for (int c2 = lane; c2 < npg_in * tcount; c2 += 32) {
-          const int hh = c2 / tcount, t = c2 - hh * tcount;
-          const int r0 = (pg0 + hh) * kRowsPerPage;
-          bulk_g2s(st + K2_V + (hh * TG + t) * kRowsPerPage * 4, p.v_in + (long long)(pos0 + t) * p.v_stride + r0,
-                   kRowsPerPage * 4, &sm.full[stage], pol_w);
-        }
-      } else if (lane == 0) {
-        bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase + pg0 * TG * kRowsPerPage, v_bytes,
-                 &sm.full[stage], pol_w);
-      }
-      if (lane == 0) {
-        trace_producer(p, seq, t_it, t_ready, 2, bytes);
-        if (p.trace && seq < p.trace_cap) {
-          p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 6] = unit;
-          p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 7] = (np << 8) | tcount;
-        }
-      }
-      __syncwarp();
-    }
+    if (nunit >= 0) fetch(nunit, nup, na, nb, nrdy);
+    if (up.kind == KIND_SHRINK)
+      seq = issue_shrink<T>(p, sm, seq, waited, up.job, da, db);
+    else
+      seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, da, db, rdy, unit);
     unit = nunit;
+    up = nup;
     da = na;
     db = nb;
     rdy = nrdy;
@@ -1021,8 +1070,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
   } else if (warp == GROUP_WARPS) {
     bool waited = false;
     int seq = 0;
-    if (mode != MODE_EXPAND) seq = produce_shrink<T>(p, sm, seq, waited);
-    if (mode != MODE_SHRINK) seq = produce_expand<T>(p, sm, seq, waited, fused);
+    seq = produce_all<T>(p, sm, seq, waited, mode);
     if (!waited) pdl_wait();
     if (lane == 0) post_marker(sm, seq, KIND_END);
   } else {

@@ -163,7 +163,6 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_ctr);
     cudaFree(pool->d_vws);
     cudaFree(pool->d_plan);
-    cudaFree(pool->d_pws);
     cudaFree(pool->d_pvimg);
     cudaFree(pool->d_pctr);
     delete pool;
@@ -191,8 +190,6 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     e = cudaMalloc(&pool->d_plan, cham_plan_bytes_internal(pool));
   }
   if (e == cudaSuccess && pool->prefill_ok)
-    e = cudaMalloc(&pool->d_pws, sizeof(float) * (size_t)kMaxJobs * kPrefillMaxSplit * max_tokens * kPrefillMaxRank);
-  if (e == cudaSuccess && pool->prefill_ok)
     e = cudaMalloc(&pool->d_pvimg, (size_t)kMaxJobs * kPrefillMaxTiles * kPrefillVImg);
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMalloc(&pool->d_pctr, sizeof(int) * prefill_ctr_ints());
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMemset(pool->d_pctr, 0, sizeof(int) * prefill_ctr_ints());
@@ -216,7 +213,6 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_ctr);
   cudaFree(pool->d_vws);
   cudaFree(pool->d_plan);
-  cudaFree(pool->d_pws);
   cudaFree(pool->d_pvimg);
   cudaFree(pool->d_pctr);
   delete pool;

@@ -38,8 +38,7 @@ struct cham_pool {
   int prefill_min_tokens = 0;          // 0 = tcgen05 path disabled
   int route_min_seg = 0;               // host hints about the next steps' segment lengths
   int route_max_seg = 1 << 30;
-  float* d_pws = nullptr;              // prefill shrink partials [kMaxJobs][ks][max_tokens][128]
-  char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB]
+  char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB] (ks partials)
   int* d_pctr = nullptr;               // prefill counters: 2 parity sets + tile V flags
   int prefill_epoch = 0;               // prefill launches so far (tile flags, counter parity)
 };

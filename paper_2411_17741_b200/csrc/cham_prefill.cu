@@ -43,11 +43,13 @@ constexpr int CW = 512;                 // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
 constexpr int MAX_TILES = kPrefillMaxTiles;
-constexpr int NTHREADS = 192;           // warps 0-3 epilogue, 4 loader, 5 MMA
+constexpr int NTHREADS = 384;           // warps 0-7 epilogue (two sets of 4), 8 loader, 9 MMA, 10-11 publishers
+constexpr int W_LOAD = 8, W_MMA = 9, W_PUB = 10;
+constexpr int PQN = 8;                  // publish ring depth per epilogue set
 constexpr int TMEM_COLS = 512;
 constexpr int TM_SH = 192;              // shrink accumulator stride: [0,192) and [192,384)
 constexpr int TM_EX = 384;              // expand accumulators: [384,448) and [448,512)
-constexpr int BAR_EPI = 1;              // named barrier of the 128 epilogue threads
+constexpr int BAR_EPI = 1;              // named barriers 1, 2: the 128 threads of epilogue set 0, 1
 
 enum Mode { MODE_FUSED = 0, MODE_SHRINK = 1, MODE_EXPAND = 2 };
 
@@ -84,10 +86,7 @@ struct alignas(64) Params {
   int epoch;               // launch id (tile V flags), parity selects the counter set
   int* ctr;                // this parity's counters: [0] dispatch, [1] finished CTAs, [2] error
   int* tile_cnt;           // this parity's split-K arrival counters [MAX_TILES]
-  int* vready;             // [MAX_TILES] tile V flags (= epoch when the V images are final)
   int* err;
-  float* part;             // fp32 shrink partials [job][kq][position][MAXR]
-  long long part_job, part_ks;
   char* vimg;              // V images [job][tile][VBUF]
   float* v_out;            // MODE_SHRINK: v [position][v_stride]
   const float* v_in;       // MODE_EXPAND: v [position][v_stride]
@@ -173,10 +172,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// debug timeline: field 0 loader claim, 1 loader issued, 2 MMA start, 3 MMA issued,
-// 4 epilogue start, 5 epilogue end, 6 unit id, 7 kind
+// debug timeline: field 0 loader claim, 1 loader issued, 2 MMA first stage ready, 3 MMA
+// issued, 4 epilogue accumulators ready, 5 epilogue end, 6 unit id | kind << 32, 7 loader
+// got the unit's first ring slot
 __device__ __forceinline__ void trace_put(const Params& p, int k, int field, unsigned long long v) {
   if (p.trace && k < p.trace_cap) p.trace[((long long)blockIdx.x * p.trace_cap + k) * 8 + field] = v;
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -187,6 +190,7 @@ struct Tile {
   int m;     // rows (<= 128)
   int slot;
   int rank;
+  int ks;    // shrink K-split of this tile (its ks partial V images must fit one V buffer)
 };
 struct TileList {
   int n_tiles;
@@ -258,7 +262,14 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
   int carry = 0;
   for (int base = 0; base < tiles; base += 32) {
     const int t = base + lane;
-    const int u = t < tiles ? (p.mode == MODE_EXPAND ? 1 : ks * n_groups(p, tl.t[t].rank)) : 0;
+    int u = 0;
+    if (t < tiles) {
+      int kt = ks;
+      const int img = ((rpad(tl.t[t].rank) + 63) / 64) * mpad(tl.t[t].m) * 128;
+      while (kt > 1 && kt * img > VBUF) kt >>= 1;
+      tl.t[t].ks = kt;
+      u = p.mode == MODE_EXPAND ? 1 : kt * n_groups(p, tl.t[t].rank);
+    }
     int inc = u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -297,6 +308,8 @@ struct Unit {
   int ngrp;           // expand: 64-column groups in the unit
   int kpc, nst;       // chunks (shrink) / groups (expand) per stage, stages
   int nchunks;        // shrink: k-chunks in the unit
+  int ks;             // the tile's K-split (expand: partial V images to accumulate)
+  int vstride;        // bytes of one partial V image (K-blocks x mp rows x 128 B)
   int xb;             // bytes of one activation chunk/group in smem (mp rows x 128 B)
   int bstride;        // expand: bytes of one group's B slices (np rounded up to even, x 1 KiB)
 };
@@ -325,12 +338,14 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
   x.np = (t.rank + 7) / 8;
   x.xb = x.mp * 128;
   x.bstride = (x.rp / 8) * kAtomBytes;
+  x.ks = t.ks;
+  x.vstride = ((x.rp + 63) / 64) * x.xb;
   if (x.kind == 1) {
     const int rem = u - tl.sh_start[x.tile];
-    x.kq = rem % tl.ks;
+    x.kq = rem % t.ks;
     x.jps = jobs_per_group(p, t.rank);
-    x.job0 = (rem / tl.ks) * x.jps;
-    x.nchunks = (p.h_in / 64) / tl.ks;
+    x.job0 = (rem / t.ks) * x.jps;
+    x.nchunks = (p.h_in / 64) / t.ks;
     const int chunk_bytes = x.xb + x.jps * (x.rp / 8) * kAtomBytes;
     x.kpc = max(1, min(4, min(STAGE / chunk_bytes, x.nchunks)));
     x.nst = (x.nchunks + x.kpc - 1) / x.kpc;
@@ -370,6 +385,35 @@ __device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileLis
   }
   return f;
 }
+#ifndef CHAM_WARM_L2
+#define CHAM_WARM_L2 0  // A/B on C3: 461.7k (on) vs 520.8k tok/s (off)
+#endif
+constexpr bool kWarmL2 = CHAM_WARM_L2 != 0;
+// Warm L2 with a unit's operands as long contiguous runs (one x/y row range per token, one
+// run of atoms per adapter page): the TMA box loads then move 128-byte row pieces out of L2
+// instead of scattering 128-byte requests over DRAM pages.
+__device__ __forceinline__ void warm_l2(const Params& p, const Unit& u, const Prefetch& f, int lane) {
+  if (u.kind == 1) {
+    const int kc0 = u.kq * u.nchunks;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (b * 32 + lane < u.m)
+        bulk_prefetch_l2(p.jobs[u.job0].x + ((long long)f.rows[b] * p.h_in + kc0 * 64) * 2, u.nchunks * 128);
+    if (lane < u.np)
+      for (int j = 0; j < u.jps; ++j)
+        bulk_prefetch_l2(p.base + (long long)f.page * p.page_bytes + p.jobs[u.job0 + j].a_off + (long long)kc0 * kAtomBytes,
+                         u.nchunks * kAtomBytes);
+  } else if (u.kind == 2) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (b * 32 + lane < u.m)
+        bulk_prefetch_l2(p.jobs[u.job].y + ((long long)f.rows[b] * p.h_out + u.col0) * 2, u.ngrp * 128);
+    if (lane < u.np)
+      bulk_prefetch_l2(p.base + (long long)f.page * p.page_bytes + p.jobs[u.job].b_off + (long long)(u.col0 / 64) * kAtomBytes,
+                       u.ngrp * kAtomBytes);
+  }
+}
+
 // Token row of block `blk` for this lane; `contig` = the block's rows are consecutive tokens
 // (one TMA box), else each lane moves its own row.
 __device__ __forceinline__ int block_row(const Prefetch& f, const Unit& u, int blk, int lane, bool& contig) {
@@ -384,16 +428,25 @@ __device__ __forceinline__ int block_row(const Prefetch& f, const Unit& u, int b
 struct Shared {
   alignas(1024) unsigned char ring[NS][STAGE];
   alignas(1024) unsigned char vbuf[2][VBUF];
+  // the UMMA A operand always spans 128 rows: the rows past a partial image's mp rows are
+  // read (and ignored) from whatever follows it, which must still be shared memory
+  unsigned char vpad[BM * 128 - 4096];
   uint64_t full[NS], empty[NS];
   uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[2], tempty_ex[2];
   uint64_t vfull[2], vempty[2];
   uint64_t ufull[UQ], uempty[UQ];
   int uslot[UQ];
   uint32_t tmem_base;
-  int last;
+  int last[2];
   int flag;
+  // epilogue set es -> publisher warp W_PUB + es: finished shrink units / V images
+  int pq_tile[2][PQN];
+  int pq_kind[2][PQN];  // 0 end, 1 split-K partials written (count, last one reduces), 2 V written
+  uint64_t pq_full[2][PQN], pq_empty[2][PQN];
   TileList tl;
 };
+
+static_assert(sizeof(Shared) <= 227 * 1024, "prefill kernel shared memory exceeds the 227 KiB per-CTA limit");
 
 // V image of (job, tile): K-block b (64 ranks) of row r, 16-byte chunk c at
 // b * mp*128 + r*128 + ((c ^ r) & 7) * 16 — the K-major SWIZZLE_128B A-operand layout.
@@ -418,13 +471,38 @@ __device__ __forceinline__ void write_v_chunk(char* img, const Unit& u, int r, i
   }
 }
 
-// Epilogue: the tile's V images are final -> publish the tile flag (release).
-__device__ __forceinline__ void publish_tile(const Params& p, int tile, int et) {
+// Epilogue set -> its publisher warp.  The set's partial / V stores precede the post through
+// the set's named barrier (CTA-scope ordering) and the release of pq_full; the publisher's
+// gpu-scope fences are cumulative, so the epilogue warps never wait on a store round trip.
+__device__ __forceinline__ void post_event(Shared& sm, int es, int& npost, int tile, int kind, int et) {
   asm volatile("fence.proxy.async.global;" ::: "memory");  // this thread's V stores -> TMA reads
-  named_bar_sync(BAR_EPI, 128);
+  named_bar_sync(BAR_EPI + es, 128);
   if (et == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.vready + tile), "r"(p.epoch) : "memory");
+    const int k = npost;
+    const int q = k % PQN;
+    if (k >= PQN) mbar_wait(&sm.pq_empty[es][q], ((k / PQN) - 1) & 1);
+    sm.pq_tile[es][q] = tile;
+    sm.pq_kind[es][q] = kind;
+    mbar_arrive(&sm.pq_full[es][q]);
+  }
+  ++npost;
+}
+
+// Publisher warp: one finished phase-1 unit (its partial V image written) -> tile counter
+// += 1 (release).  Expand units of the tile wait for all of the tile's units.
+__device__ void publisher(const Params& p, Shared& sm, int es) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0;; ++k) {
+    const int q = k % PQN;
+    mbar_wait(&sm.pq_full[es][q], (k / PQN) & 1);
+    const int tile = sm.pq_tile[es][q], kind = sm.pq_kind[es][q];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.pq_empty[es][q]);
+    if (kind == 0) break;
+    if (lane == 0) {
+      __threadfence();  // cumulative over the epilogue set's image stores
+      red_release_gpu_add(p.tile_cnt + tile, 1);
+    }
   }
 }
 
@@ -436,7 +514,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 1 + 4);  // MMA commit + one arrival per epilogue warp
+      mbar_init(&sm.empty[i], 1 + 8);  // MMA commit + one arrival per epilogue warp
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull_sh[i], 1);
@@ -448,17 +526,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     }
     for (int i = 0; i < UQ; ++i) {
       mbar_init(&sm.ufull[i], 1);
-      mbar_init(&sm.uempty[i], 1 + 4);
+      mbar_init(&sm.uempty[i], 1 + 8);
     }
+    for (int e = 0; e < 2; ++e)
+      for (int i = 0; i < PQN; ++i) {
+        mbar_init(&sm.pq_full[e][i], 1);
+        mbar_init(&sm.pq_empty[e][i], 1);
+      }
     fence_mbar_init();
   }
-  if (warp == 4 && lane < p.n_jobs) {
+  if (warp == W_LOAD && lane < p.n_jobs) {
     prefetch_map(&p.maps[lane].x32);
     prefetch_map(&p.maps[lane].x1);
     prefetch_map(&p.maps[lane].y32);
     prefetch_map(&p.maps[lane].y1);
   }
-  if (warp == 5) {
+  if (warp == W_MMA) {
     tmem_alloc(&sm.tmem_base);
     tc_fence_before();
   }
@@ -471,7 +554,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   pdl_launch_dependents();
   if (!sm.flag) {
     if (tid == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
-  } else if (warp == 4) {
+  } else if (warp == W_LOAD) {
     // ---------------------------------------------------------------- loader + dispatch
     const uint64_t pol_w = policy_evict_first();  // adapter pages: streamed
     const uint64_t pol_x = policy_evict_last();   // x: re-read by the other job groups / K ranges
@@ -479,18 +562,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     int next = blockIdx.x;  // first unit static, the rest from the counter (one claim ahead)
     int claim = 0;
     if (lane == 0 && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
-    // tile V flag of an expand unit, read without blocking one unit ahead
+    // published phase-1 units of an expand unit's tile, read without blocking one unit ahead
     const int ex_per_tile = p.n_jobs * ((p.h_out + CW - 1) / CW);
     auto peek_flag = [&](int u) {
       int v = 0;
       if (lane == 0 && u >= tl.u1 && u < tl.u_total) {
-        const int* f = p.vready + (u - tl.u1) / ex_per_tile;
+        const int* f = p.tile_cnt + (u - tl.u1) / ex_per_tile;
         asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       }
       return v;
     };
     int flag = peek_flag(next);
     Prefetch pf = prefetch_unit(p, tl, next, lane);
+    if (kWarmL2 && next < tl.u_total) warm_l2(p, make_unit(p, tl, next), pf, lane);
     int seq = 0, nex = 0;
     for (int k = 0;; ++k) {
       if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 1, gtimer());
@@ -512,8 +596,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       const Unit u = make_unit(p, tl, u_id);
       if (lane == 0 && p.trace) {
         trace_put(p, k, 0, gtimer());
-        trace_put(p, k, 6, u_id);
-        trace_put(p, k, 7, u.kind);
+        trace_put(p, k, 6, (unsigned long long)u_id | ((unsigned long long)u.kind << 32));
       }
       if (u.kind == 3) continue;
       const int my_page = cf.page;
@@ -531,6 +614,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int c_first = s * u.kpc;
           const int nch = min(u.kpc, u.nchunks - c_first);
           if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
+          if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
           uint32_t bytes = nch * n_cp * kAtomBytes;
 #pragma unroll
           for (int b = 0; b < 4; ++b)
@@ -567,10 +651,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         const int vb = nex & 1;
         if (lane == 0) {
           if (nex >= 2) mbar_wait(&sm.vempty[vb], ((nex >> 1) - 1) & 1);
-          if (cur_flag != p.epoch)
-            while (ld_acquire_gpu(p.vready + u.tile) != p.epoch) __nanosleep(32);
+          // every phase-1 unit of the tile has published its partial V image
+          const int need = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
+          if (cur_flag < need)
+            while (ld_acquire_gpu(p.tile_cnt + u.tile) < need) __nanosleep(32);
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          const uint32_t vbytes = ((u.rp + 63) / 64) * u.xb;
+          const uint32_t vbytes = u.ks * u.vstride;
           mbar_arrive_expect_tx(&sm.vfull[vb], vbytes);
           bulk_g2s(sm.vbuf[vb], vimg_of(p, u.job, u.tile), vbytes, &sm.vfull[vb], pol_w);
         }
@@ -587,6 +673,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int g_first = s * u.kpc;
           const int ng = min(u.kpc, u.ngrp - g_first);
           if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
+          if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
           unsigned char* stg = sm.ring[st];
           if (pad) {
             // odd page count: the K rows rank..rp of every group are a zero atom
@@ -624,8 +711,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           }
         }
       }
+      if (kWarmL2 && next < tl.u_total) warm_l2(p, make_unit(p, tl, next), pf, lane);
     }
-  } else if (warp == 5) {
+  } else if (warp >= W_PUB) {
+    publisher(p, sm, warp - W_PUB);
+  } else if (warp == W_MMA) {
     // ---------------------------------------------------------------- MMA issuer
     int seq = 0, nsh = 0, nex = 0, ngrp = 0;
     const uint32_t idesc_ex = idesc_bf16(BM, 64, true);
@@ -638,7 +728,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
       if (u_id < 0) break;
       const Unit u = make_unit(p, tl, u_id);
-      if (lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
       if (u.kind == 3) continue;
       if (u.kind == 1) {
         const int ab = nsh & 1;
@@ -649,6 +738,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int st = seq % NS;
           const int nch = min(u.kpc, u.nchunks - s * u.kpc);
           mbar_wait(&sm.full[st], (seq / NS) & 1);
+          if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
           tc_fence_after();
           if (lane == 0) {
             const uint32_t base = smem_u32(sm.ring[st]);
@@ -664,6 +754,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
               }
             }
             mma_commit(&sm.empty[st]);
+            mbar_arrive_cnt(&sm.empty[st], 8);  // the epilogue warps never read shrink stages
             if (s == u.nst - 1) mma_commit(&sm.tfull_sh[ab]);
           }
           __syncwarp();
@@ -678,6 +769,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int st = seq % NS;
           const int ng = min(u.kpc, u.ngrp - s * u.kpc);
           mbar_wait(&sm.full[st], (seq / NS) & 1);
+          if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
           tc_fence_after();
           const uint32_t base = smem_u32(sm.ring[st]);
           for (int g = 0; g < ng; ++g, ++ngrp) {
@@ -686,11 +778,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             tc_fence_after();
             if (lane == 0) {
               const uint32_t ba = base + g * u.bstride;
-              for (int kk = 0; kk < u.rp / 16; ++kk) {
-                const uint64_t ad = sdesc(va + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
-                const uint64_t bd = sdesc(ba + kk * 2 * kAtomBytes, kAtomBytes, kAtomBytes);
-                mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, kk ? 1u : 0u);
-              }
+              // D2 = sum over the tile's K-split partial images V_kq of V_kq . B
+              for (int kq = 0; kq < u.ks; ++kq)
+                for (int kk = 0; kk < u.rp / 16; ++kk) {
+                  const uint64_t ad = sdesc(va + kq * u.vstride + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
+                  const uint64_t bd = sdesc(ba + kk * 2 * kAtomBytes, kAtomBytes, kAtomBytes);
+                  mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, (kq | kk) ? 1u : 0u);
+                }
               mma_commit(&sm.tfull_ex[acc]);
             }
             __syncwarp();
@@ -705,23 +799,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue warps 0-3
-    const int r = warp * 32 + lane;  // tile row == TMEM lane
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    int seq = 0, nsh = 0, ngrp = 0;
+    // ---------------------------------------------------------------- epilogue warps 0-7
+    // Two sets of four warps (es = warp / 4), each covering all 128 rows (TMEM lane quarter
+    // = warp % 4): set es drains the shrink units with nsh % 2 == es and the expand groups
+    // with ngrp % 2 == es, i.e. exactly the TMEM accumulator buffer es.
+    const int es = warp >> 2, wq = warp & 3;
+    const int r = wq * 32 + lane;  // tile row == TMEM lane
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    int seq = 0, nsh = 0, ngrp = 0, nvb = 0, npost = 0;
     for (int k = 0;; ++k) {
-      if (k > 0 && r == 0 && p.trace) trace_put(p, k - 1, 5, gtimer());
+      if (k > 0 && tid == 0 && p.trace) trace_put(p, k - 1, 5, gtimer());
       const int q = k % UQ;
       mbar_wait(&sm.ufull[q], (k / UQ) & 1);
       const int u_id = sm.uslot[q];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
-      if (u_id < 0) break;
+      if (u_id < 0) {
+        post_event(sm, es, npost, 0, 0, r);  // the publisher exits
+        break;
+      }
       const Unit u = make_unit(p, tl, u_id);
-      if (r == 0 && p.trace) trace_put(p, k, 4, gtimer());
       const int pos = u.pos0 + min(r, u.m - 1);
       if (u.kind == 3) {
         // ---- MODE_EXPAND phase 1: caller's v rows -> V image
+        if ((nvb++ & 1) != es) continue;
         if (r < u.mp) {
           const int nv = r < u.m ? min(u.rank, p.v_stride) : 0;
           const float* src = p.v_in + (long long)pos * p.v_stride;
@@ -732,22 +833,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             write_v_chunk(vimg_of(p, 0, u.tile), u, r, c0, v, nv);
           }
         }
-        publish_tile(p, u.tile, r);
+        post_event(sm, es, npost, u.tile, 2, r);
         continue;
       }
       if (u.kind == 1) {
-        // ---- shrink: release the unit's stages, then drain the accumulators
-        for (int s = 0; s < u.nst; ++s, ++seq) {
-          const int st = seq % NS;
-          mbar_wait(&sm.full[st], (seq / NS) & 1);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.empty[st]);
-        }
+        // ---- shrink: drain the accumulators (the MMA warp releases the stages)
+        seq += u.nst;
         const int ab = nsh & 1;
+        if (ab != es) {
+          ++nsh;
+          continue;
+        }
         mbar_wait(&sm.tfull_sh[ab], (nsh >> 1) & 1);
+        if (r == 0 && p.trace) trace_put(p, k, 4, gtimer());
         tc_fence_after();
         ++nsh;
-        const bool direct = tl.ks == 1 && u.jps == p.n_jobs;  // this unit alone makes the tile's V
         for (int j = 0; j < u.jps; ++j) {
           const int job = u.job0 + j;
           for (int c0 = 0; c0 < u.rank; c0 += 32) {
@@ -761,13 +861,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
                 for (int i = 0; i < 32; ++i)
                   if (c0 + i < nv) dst[c0 + i] = v[i];
               }
-            } else if (direct) {
-              if (r < u.mp) write_v_chunk(vimg_of(p, job, u.tile), u, r, c0, v, r < u.m ? u.rank : 0);
-            } else if (r < u.m) {
-              float* dst = p.part + job * p.part_job + u.kq * p.part_ks + (long long)pos * MAXR + c0;
-#pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                if (c0 + i < u.rank) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else if (r < u.mp) {
+              // this K range's partial V image (bf16); the expand MMAs accumulate the ks images
+              write_v_chunk(vimg_of(p, job, u.tile) + u.kq * u.vstride, u, r, c0, v, r < u.m ? u.rank : 0);
             }
           }
         }
@@ -775,43 +871,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty_sh[ab]);
         if (p.mode == MODE_SHRINK) continue;
-        if (direct) {
-          publish_tile(p, u.tile, r);
-          continue;
-        }
-        // split-K / job-group arrival: the last unit of the tile reduces and publishes
-        named_bar_sync(BAR_EPI, 128);
-        if (r == 0) {
-          __threadfence();
-          const int units = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
-          sm.last = atomicAdd(p.tile_cnt + u.tile, 1) == units - 1;
-          __threadfence();
-        }
-        named_bar_sync(BAR_EPI, 128);
-        if (sm.last) {
-          for (int job = 0; job < p.n_jobs; ++job) {
-            if (r >= u.mp) continue;
-            for (int c0 = 0; c0 < u.rp; c0 += 32) {
-              float v[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0.f;
-              if (r < u.m) {
-                for (int kq = 0; kq < tl.ks; ++kq) {
-                  const float* src = p.part + job * p.part_job + kq * p.part_ks + (long long)pos * MAXR + c0;
-#pragma unroll
-                  for (int i = 0; i < 32; i += 4) {
-                    if (c0 + i < u.rank) {
-                      const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
-                      v[i] += f.x; v[i + 1] += f.y; v[i + 2] += f.z; v[i + 3] += f.w;
-                    }
-                  }
-                }
-              }
-              write_v_chunk(vimg_of(p, job, u.tile), u, r, c0, v, r < u.m ? u.rank : 0);
-            }
-          }
-          publish_tile(p, u.tile, r);
-        }
+        post_event(sm, es, npost, u.tile, 2, r);
         continue;
       }
       // ---- expand: y rows += D2 per 64-column group.  Each thread adds its row in place in
@@ -824,9 +884,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         const int st = seq % NS;
         const int ng = min(u.kpc, u.ngrp - s * u.kpc);
         mbar_wait(&sm.full[st], (seq / NS) & 1);  // the y rows of this stage have landed
+        if (s == 0 && tid == 0 && p.trace) trace_put(p, k, 4, gtimer());
         const unsigned char* ybase = sm.ring[st] + u.kpc * u.bstride;
         for (int g = 0; g < ng; ++g, ++ngrp) {
           const int acc = ngrp & 1;
+          if (acc != es) continue;  // the other set's group
           mbar_wait(&sm.tfull_ex[acc], (ngrp >> 1) & 1);
           tc_fence_after();
           float d0[32], d1[32];
@@ -858,8 +920,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             const int rr = i * 4 + (lane >> 3);  // row of this warp's block
             const int c = lane & 7;              // 16-byte chunk of the row
             const int grow = __shfl_sync(0xffffffffu, yrow_idx, rr);
-            if (warp * 32 + rr < u.m) {
-              const uint4 w = lds128(yg + swz(warp * 32 + rr, c));
+            if (wq * 32 + rr < u.m) {
+              const uint4 w = lds128(yg + swz(wq * 32 + rr, c));
               *reinterpret_cast<uint4*>(ybase_g + ((long long)grow * p.h_out + col0 + c * 8) * 2) = w;
             }
           }
@@ -871,16 +933,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   }
   // the last CTA re-arms this parity's counters
   __syncthreads();
-  if (warp == 5) {
+  if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem);
   }
   if (tid == 0) {
     __threadfence();
-    sm.last = atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1;
+    sm.last[0] = atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1;
   }
   __syncthreads();
-  if (sm.last) {
+  if (sm.last[0]) {
     for (int i = tid; i < MAX_TILES; i += NTHREADS) p.tile_cnt[i] = 0;
     if (tid == 0) {
       p.ctr[0] = 0;
@@ -963,11 +1025,7 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   int* pc = pool->d_pctr + (prm.epoch & 1) * (kPrefillCtrSet);
   prm.ctr = pc;
   prm.tile_cnt = pc + 4;
-  prm.vready = pool->d_pctr + 2 * kPrefillCtrSet;
   prm.err = pool->d_ctr + 2;
-  prm.part = pool->d_pws;
-  prm.part_ks = (long long)pool->max_tokens * MAXR;
-  prm.part_job = prm.part_ks * kPrefillMaxSplit;
   prm.vimg = pool->d_pvimg;
   prm.v_out = v_out;
   prm.v_in = v_in;

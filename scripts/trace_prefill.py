@@ -61,32 +61,40 @@ def main():
             lora_apply_table(xs[1], ys[3], ex.table, pool=pool, layer=1, proj=3)
         torch.cuda.synchronize()
         tr = buf.cpu().numpy()[1].astype(np.int64)
+        te = buf.cpu().numpy()[0].astype(np.int64)
+        np.save(out / f"trace_prefill_epi_{name}.npy", te)
         np.save(out / f"trace_prefill_{name}.npy", tr)
         valid = tr[:, :, 0] > 0
         t0 = tr[:, :, 0][valid].min()
-        rel = np.where(tr[:, :, :6] > 0, tr[:, :, :6] - t0, 0) / 1e3
-        kind = tr[:, :, 7]
+        T = np.where(tr > 0, tr - t0, 0) / 1e3
+        kind = tr[:, :, 6] >> 32
         n = valid.sum(1)
-        span = rel[:, :, 5][valid].max()
+        span = T[:, :, 5][valid].max()
         print(f"== {name}: span {span:.1f} us, units/CTA min {n.min()} max {n.max()} mean {n.mean():.1f}")
+
+        def pct(a):
+            return "p50 %.2f p90 %.2f" % (np.median(a), np.percentile(a, 90)) if len(a) else "-"
         for k, kn in ((1, "shrink"), (2, "expand"), (3, "vbuild")):
             m = valid & (kind == k)
-            m5 = m & (tr[:, :, 5] > 0) & (tr[:, :, 1] > 0) & (tr[:, :, 3] > 0)
-            if not m5.any():
+            if not m.any():
                 continue
-            ld = (rel[:, :, 1] - rel[:, :, 0])[m5]
-            mma = (rel[:, :, 3] - rel[:, :, 2])[m5]
-            epi = (rel[:, :, 5] - rel[:, :, 4])[m5]
-            lag = (rel[:, :, 5] - rel[:, :, 0])[m5]
-            print(f"  {kn}: n={m.sum()} loader issue us p50 {np.median(ld):.2f} p90 {np.percentile(ld, 90):.2f}; "
-                  f"MMA p50 {np.median(mma):.2f}; epilogue p50 {np.median(epi):.2f} p90 {np.percentile(epi, 90):.2f}; "
-                  f"claim->epilogue end p50 {np.median(lag):.2f}")
-            print(f"     first claim {rel[:, :, 0][m].min():.1f} us, last epilogue end {rel[:, :, 5][m5].max():.1f} us")
-        fin = np.array([rel[c, :n[c], 5].max() if n[c] else 0 for c in range(sm)])
+            ok = m & (tr[:, :, 7] > 0) & (tr[:, :, 1] > 0)
+            print(f"  {kn}: n={m.sum()}  first claim {T[:, :, 0][m].min():.1f} us, last claim {T[:, :, 0][m].max():.1f} us")
+            print(f"    loader: claim->first slot {pct((T[:, :, 7] - T[:, :, 0])[ok])}; first slot->all issued {pct((T[:, :, 1] - T[:, :, 7])[ok])}")
+            ok2 = m & (tr[:, :, 2] > 0) & (tr[:, :, 3] > 0) & (tr[:, :, 7] > 0)
+            print(f"    MMA: slot->first stage full {pct((T[:, :, 2] - T[:, :, 7])[ok2])}; first full->last MMA issued {pct((T[:, :, 3] - T[:, :, 2])[ok2])}")
+            ok3 = m & (tr[:, :, 4] > 0) & (tr[:, :, 5] > 0)
+            print(f"    epilogue: acc ready->end {pct((T[:, :, 5] - T[:, :, 4])[ok3])}")
+        E = np.where(te > 0, te - t0, 0) / 1e3
+        me = (kind == 1) & (te[:, :, 0] > 0) & (te[:, :, 3] > 0)
+        if me.any():
+            print(f"    shrink epi detail: acc->drained {pct((E[:, :, 0] - T[:, :, 4])[me])}; drained->bar1 {pct((E[:, :, 1] - E[:, :, 0])[me])}; "
+                  f"bar1->atomic {pct((E[:, :, 2] - E[:, :, 1])[me])}; atomic->bar2 {pct((E[:, :, 3] - E[:, :, 2])[me])}")
+        ml = me & (te[:, :, 5] > 0)
+        if ml.any():
+            print(f"    last-arriver: bar2->reduced {pct((E[:, :, 4] - E[:, :, 3])[ml])}; reduced->published {pct((E[:, :, 5] - E[:, :, 4])[ml])}")
+        fin = np.array([T[c, :n[c], 5].max() if n[c] else 0 for c in range(sm)])
         print(f"  CTA finish us min {fin.min():.1f} p50 {np.median(fin):.1f} max {fin.max():.1f}")
-        # per-CTA loader busy fraction: sum of issue spans / span
-        busy = np.where(valid & (tr[:, :, 1] > 0), rel[:, :, 1] - rel[:, :, 0], 0).sum(1)
-        print(f"  loader issue time per CTA us p50 {np.median(busy):.1f} (of span {span:.1f})")
     _lib.call("cham_debug_set_trace", pool.handle, None, 0)
 
 
