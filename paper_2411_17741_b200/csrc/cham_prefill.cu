@@ -60,10 +60,10 @@ struct Job {
   long long b_off;
 };
 
-// Activation tensor maps of one job: a 64-column x 32-row box for contiguous rows and a
+// Activation tensor maps of one job: a 64-column x 64-row box for contiguous rows and a
 // 64-column x 1-row box for gathered ones, both SWIZZLE_128B (x for shrink, y for expand).
 struct alignas(64) Maps {
-  CUtensorMap x32, x1, y32, y1;
+  CUtensorMap x64, x1, y64, y1;
 };
 
 struct alignas(64) Params {
@@ -202,7 +202,7 @@ struct TileList {
 };
 
 __host__ __device__ __forceinline__ int rpad(int rank) { return (rank + 15) & ~15; }
-__host__ __device__ __forceinline__ int mpad(int m) { return (m + 31) & ~31; }
+__host__ __device__ __forceinline__ int mpad(int m) { return (m + 63) & ~63; }  // 64-row TMA boxes
 // jobs sharing one shrink stage: all of them when their A^T atoms fit a 16 KiB region
 __device__ __forceinline__ int jobs_per_group(const Params& p, int rank) {
   return (p.mode == MODE_FUSED && p.x_shared && p.n_jobs * (rpad(rank) / 8) <= 16) ? p.n_jobs : 1;
@@ -414,6 +414,15 @@ __device__ __forceinline__ void warm_l2(const Params& p, const Unit& u, const Pr
   }
 }
 
+// 64-row block h of the tile: one TMA box when its (up to) 64 valid rows are consecutive tokens
+__device__ __forceinline__ bool block64(const bool (&contig)[4], const int (&rows)[4], int nblk, int h) {
+  bool ok = contig[2 * h];
+  if (2 * h + 1 < nblk)
+    ok = ok && contig[2 * h + 1] &&
+         __shfl_sync(0xffffffffu, rows[2 * h + 1], 0) == __shfl_sync(0xffffffffu, rows[2 * h], 0) + 32;
+  return ok;
+}
+
 // Token row of block `blk` for this lane; `contig` = the block's rows are consecutive tokens
 // (one TMA box), else each lane moves its own row.
 __device__ __forceinline__ int block_row(const Prefetch& f, const Unit& u, int blk, int lane, bool& contig) {
@@ -536,9 +545,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     fence_mbar_init();
   }
   if (warp == W_LOAD && lane < p.n_jobs) {
-    prefetch_map(&p.maps[lane].x32);
+    prefetch_map(&p.maps[lane].x64);
     prefetch_map(&p.maps[lane].x1);
-    prefetch_map(&p.maps[lane].y32);
+    prefetch_map(&p.maps[lane].y64);
     prefetch_map(&p.maps[lane].y1);
   }
   if (warp == W_MMA) {
@@ -607,18 +616,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         int rows[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(cf, u, b, lane, contig[b]) : 0;
+        const bool c64[2] = {block64(contig, rows, nblk, 0), nblk > 2 && block64(contig, rows, nblk, 1)};
         const int kc0 = u.kq * u.nchunks;
-        const int n_cp = u.jps * u.np;  // A copies per chunk
+        const int np_pad = u.rp / 8;
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
           const int c_first = s * u.kpc;
           const int nch = min(u.kpc, u.nchunks - c_first);
           if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
-          uint32_t bytes = nch * n_cp * kAtomBytes;
+          uint32_t bytes = nch * u.jps * u.np * kAtomBytes;
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (b < nblk) bytes += nch * (contig[b] ? 32 * 128 : min(32, u.m - b * 32) * 128);
+          for (int h = 0; h < 2; ++h)
+            if (h * 64 < u.m) bytes += nch * (c64[h] ? 64 * 128 : min(64, u.m - h * 64) * 128);
           if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
           __syncwarp();
           unsigned char* stg = sm.ring[st];
@@ -626,23 +636,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             const int kc = kc0 + c_first + i;
             unsigned char* xdst = stg + i * u.xb;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              if (b >= nblk) continue;
-              if (contig[b]) {
+            for (int h = 0; h < 2; ++h) {
+              if (h * 64 >= u.m) continue;
+              if (c64[h]) {
                 if (lane == 0)
-                  tma_load_2d(xdst + b * 32 * 128, &p.maps[u.job0].x32, kc * 64, rows[b], &sm.full[st], pol_x);
-              } else if (b * 32 + lane < u.m) {
-                tma_load_2d(xdst + (b * 32 + lane) * 128, &p.maps[u.job0].x1, kc * 64, rows[b], &sm.full[st], pol_x);
+                  tma_load_2d(xdst + h * 64 * 128, &p.maps[u.job0].x64, kc * 64, rows[2 * h], &sm.full[st], pol_x);
+              } else {
+#pragma unroll
+                for (int b = 2 * h; b < 2 * h + 2; ++b)
+                  if (b * 32 + lane < u.m)
+                    tma_load_2d(xdst + (b * 32 + lane) * 128, &p.maps[u.job0].x1, kc * 64, rows[b], &sm.full[st], pol_x);
               }
             }
-            unsigned char* adst = stg + u.kpc * u.xb + i * u.jps * u.bstride;
-            // lanes 0..np-1 hold the page ids; copy job by job
-            for (int j = 0; j < u.jps; ++j) {
-              if (lane < u.np) {
-                const char* src = p.base + (long long)my_page * p.page_bytes + p.jobs[u.job0 + j].a_off +
-                                  (long long)kc * kAtomBytes;
-                bulk_g2s(adst + j * u.bstride + lane * kAtomBytes, src, kAtomBytes, &sm.full[st], pol_w);
-              }
+          }
+          // A^T atoms [job][page][chunk]: one copy of the stage's nch chunks per (job, page)
+          unsigned char* adst = stg + u.kpc * u.xb;
+          for (int j = 0; j < u.jps; ++j) {
+            if (lane < u.np) {
+              const char* src = p.base + (long long)my_page * p.page_bytes + p.jobs[u.job0 + j].a_off +
+                                (long long)(kc0 + c_first) * kAtomBytes;
+              bulk_g2s(adst + (j * np_pad + lane) * u.kpc * kAtomBytes, src, nch * kAtomBytes, &sm.full[st], pol_w);
             }
           }
         }
@@ -667,6 +680,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         int rows[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(cf, u, b, lane, contig[b]) : 0;
+        const bool c64[2] = {block64(contig, rows, nblk, 0), nblk > 2 && block64(contig, rows, nblk, 1)};
         const bool pad = (u.rp / 8) > u.np;
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
@@ -676,36 +690,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
           unsigned char* stg = sm.ring[st];
           if (pad) {
-            // odd page count: the K rows rank..rp of every group are a zero atom
-            for (int g = 0; g < ng; ++g) {
-              uint4* z = reinterpret_cast<uint4*>(stg + g * u.bstride + u.np * kAtomBytes);
-              z[lane] = make_uint4(0, 0, 0, 0);
-              z[lane + 32] = make_uint4(0, 0, 0, 0);
-            }
+            // odd page count: the K rows rank..rp of every group are a zero atom (page np)
+            for (int c = lane; c < ng * 64; c += 32)
+              reinterpret_cast<uint4*>(stg + u.np * u.kpc * kAtomBytes)[c] = make_uint4(0, 0, 0, 0);
             fence_proxy_async_shared();
           }
           __syncwarp();
           uint32_t bytes = ng * u.np * kAtomBytes;
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (b < nblk) bytes += ng * (contig[b] ? 32 * 128 : min(32, u.m - b * 32) * 128);
+          for (int h = 0; h < 2; ++h)
+            if (h * 64 < u.m) bytes += ng * (c64[h] ? 64 * 128 : min(64, u.m - h * 64) * 128);
           if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
           __syncwarp();
+          // B atoms [page][group]: one copy of the stage's ng groups per page
+          if (lane < u.np) {
+            const char* src = p.base + (long long)my_page * p.page_bytes + p.jobs[u.job].b_off +
+                              (long long)(u.col0 / 64 + g_first) * kAtomBytes;
+            bulk_g2s(stg + lane * u.kpc * kAtomBytes, src, ng * kAtomBytes, &sm.full[st], pol_w);
+          }
           for (int g = 0; g < ng; ++g) {
             const int col = u.col0 + (g_first + g) * 64;
-            if (lane < u.np) {
-              const char* src = p.base + (long long)my_page * p.page_bytes + p.jobs[u.job].b_off +
-                                (long long)(col / 64) * kAtomBytes;
-              bulk_g2s(stg + g * u.bstride + lane * kAtomBytes, src, kAtomBytes, &sm.full[st], pol_w);
-            }
             unsigned char* ydst = stg + u.kpc * u.bstride + g * u.xb;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              if (b >= nblk) continue;
-              if (contig[b]) {
-                if (lane == 0) tma_load_2d(ydst + b * 32 * 128, &p.maps[u.job].y32, col, rows[b], &sm.full[st], pol_y);
-              } else if (b * 32 + lane < u.m) {
-                tma_load_2d(ydst + (b * 32 + lane) * 128, &p.maps[u.job].y1, col, rows[b], &sm.full[st], pol_y);
+            for (int h = 0; h < 2; ++h) {
+              if (h * 64 >= u.m) continue;
+              if (c64[h]) {
+                if (lane == 0) tma_load_2d(ydst + h * 64 * 128, &p.maps[u.job].y64, col, rows[2 * h], &sm.full[st], pol_y);
+              } else {
+#pragma unroll
+                for (int b = 2 * h; b < 2 * h + 2; ++b)
+                  if (b * 32 + lane < u.m)
+                    tma_load_2d(ydst + (b * 32 + lane) * 128, &p.maps[u.job].y1, col, rows[b], &sm.full[st], pol_y);
               }
             }
           }
@@ -745,11 +760,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             for (int i = 0; i < nch; ++i) {
               const uint32_t xa = base + i * u.xb;
               for (int j = 0; j < u.jps; ++j) {
-                const uint32_t aa = base + u.kpc * u.xb + (i * u.jps + j) * u.bstride;
+                // A^T atoms [job][page][chunk]: the pages of chunk i are kpc atoms apart
+                const uint32_t aa = base + u.kpc * u.xb + (j * (u.rp / 8) * u.kpc + i) * kAtomBytes;
                 const uint32_t d = tmem + ab * TM_SH + j * u.rp;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  mma_bf16(d, sdesc(xa + kk * 32, 16, 1024), sdesc(aa + kk * 32, 16, kAtomBytes), idesc,
+                  mma_bf16(d, sdesc(xa + kk * 32, 16, 1024), sdesc(aa + kk * 32, 16, u.kpc * kAtomBytes), idesc,
                            (s | i | kk) ? 1u : 0u);
               }
             }
@@ -777,12 +793,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             if (ngrp >= 2) mbar_wait(&sm.tempty_ex[acc], ((ngrp >> 1) - 1) & 1);
             tc_fence_after();
             if (lane == 0) {
-              const uint32_t ba = base + g * u.bstride;
+              const uint32_t ba = base + g * kAtomBytes;  // B atoms [page][group]
               // D2 = sum over the tile's K-split partial images V_kq of V_kq . B
               for (int kq = 0; kq < u.ks; ++kq)
                 for (int kk = 0; kk < u.rp / 16; ++kk) {
                   const uint64_t ad = sdesc(va + kq * u.vstride + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
-                  const uint64_t bd = sdesc(ba + kk * 2 * kAtomBytes, kAtomBytes, kAtomBytes);
+                  const uint64_t bd = sdesc(ba + kk * 2 * u.kpc * kAtomBytes, kAtomBytes, u.kpc * kAtomBytes);
                   mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, (kq | kk) ? 1u : 0u);
                 }
               mma_commit(&sm.tfull_ex[acc]);
@@ -1037,11 +1053,11 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   for (int j = 0; j < n_jobs; ++j) {
     int rc = CHAM_OK;
     if (mode != MODE_EXPAND) {
-      rc = encode_act_map(&prm.maps[j].x32, xs[j], n_tokens, prm.h_in, 32);
+      rc = encode_act_map(&prm.maps[j].x64, xs[j], n_tokens, prm.h_in, 64);
       if (!rc) rc = encode_act_map(&prm.maps[j].x1, xs[j], n_tokens, prm.h_in, 1);
     }
     if (!rc && mode != MODE_SHRINK) {
-      rc = encode_act_map(&prm.maps[j].y32, ys[j], n_tokens, prm.h_out, 32);
+      rc = encode_act_map(&prm.maps[j].y64, ys[j], n_tokens, prm.h_out, 64);
       if (!rc) rc = encode_act_map(&prm.maps[j].y1, ys[j], n_tokens, prm.h_out, 1);
     }
     if (rc) return rc;
