@@ -62,6 +62,15 @@ def algorithmic_bytes(seg_off, seg_slot, seg_rank, n_tokens, h_in, h_out, es):
     return adapter, act
 
 
+def traffic_per_launch(config: str):
+    """DRAM bytes per apply launch from the committed ncu --set full summary (scripts/ncu_summary.py),
+    or None when no capture of this config is committed."""
+    p = ROOT / "profiles" / f"traffic_{config}.json"
+    if not p.exists():
+        return None
+    return float(json.loads(p.read_text())["traffic_per_launch"])
+
+
 # --------------------------------------------------------------------------- clocks sampler
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -319,11 +328,11 @@ def run_ours(args, rank: int, world: int):
         if args.config == "c3":
             workload = ("C3: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers) prefill, 64 segments x 64 tokens over "
                         "64 adapters with power-law ranks (prefill_batch seed = rank), tcgen05 path")
-            kernels = "prefill::shrink_kernel + prefill::expand_kernel (tcgen05, TMEM accumulators) per apply"
+            kernels = "prefill::fused_kernel (tcgen05, TMEM accumulators; shrink -> per-tile V images -> expand, PDL-chained) per apply"
         else:
             workload = ("C2: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers), 100 adapters ranks 8-128, "
                         "decode batch 256 tokens per GPU (assign_adapter seed = rank)")
-            kernels = "decode::lora_apply_kernel<bf16> (fused shrink -> grid barrier -> expand, PDL-chained)"
+            kernels = "decode::lora_apply_kernel<bf16> (shrink and expand units from one queue, per-tile v-ready counters, PDL-chained)"
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -339,8 +348,11 @@ def run_ours(args, rank: int, world: int):
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "kernel": kernels,
                          "bytes_per_step": bytes_step, "launches_per_step": apply_launches,
+                         "algorithmic_bytes_per_launch": bytes_step / apply_launches,
                          "avg_launch_us": apply_ms * 1e3 / apply_launches,
-                         "traffic": None},
+                         "traffic": traffic_per_launch(args.config),
+                         "traffic_source": "profiles/traffic_%s.json (ncu --set full, cold L2, DRAM read+write "
+                                           "bytes per launch, mean of one q/k/v and one o launch)" % args.config},
             "flops_per_step": flops_step,
             "tensor_frac_of_peak": flops_step / (apply_ms * 1e-3) / 1e12 / bf16_peak,
             "e2e": {"value": tokens_total / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d,

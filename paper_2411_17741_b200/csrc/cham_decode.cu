@@ -126,6 +126,9 @@ struct Params {
   const int* n_seg_dev;
   int* ctr;        // [0] next shrink unit, [1] finished CTAs, [4] next expand unit
   int* tile_ctr;   // MODE_FUSED: [job][expand tile] shrink units finished (v rows published)
+  float* split_buf;   // page-half partials [job][split tile][col chunk][TG][cols of a chunk]
+  int* split_ctr;     // [job][split tile][col chunk]: half 0 published its partial
+  int split_ncc;      // column chunks per split tile (scratch geometry)
   int* err;
   float* vws;      // this apply's compact v buffer: [job][sum_s T_s * rpad_s]
   long long vws_job_stride;
@@ -155,6 +158,8 @@ struct Meta {
   int ncb;    // K2: bytes of one B row in this unit
   int pitch;  // K2: page pitch in the stage
   int nq;     // K2: 16-byte column chunks in this unit
+  int xm;     // K2: 0 plain, 1 page half 0 (write partial), 2 page half 1 (combine stage last)
+  int sidx;   // K2: split scratch / flag slot
   int rows[TG];
 };
 
@@ -175,6 +180,7 @@ struct alignas(16) Plan {
   int sh_lpt[PLAN_SEGS + 1];  // K1 unit prefix by LPT position
   int cls_pos[kMaxPagesPerSlot + 2];  // LPT positions where the page-count classes start
   int n_cls;
+  int n_split;  // leading LPT expand tiles split into page halves (np > kSplitNp)
   int order_pos[PLAN_SEGS];  // segment -> position in the LPT order
   long long desc_cap;        // descriptor capacity (entries) after the header
 };
@@ -197,6 +203,15 @@ __host__ __device__ inline long long plan_desc_capacity(int max_tokens) {
 }
 
 constexpr int MAX_BLOCKS = 2 * (kMaxPagesPerSlot + 1);
+// Expand units of tiles whose adapter has more than kSplitNp pages are split into two page
+// halves: half 0 leaves its fp32 partial sums in a scratch slot, half 1 adds them (plus its
+// own and y) in a final combine stage.  Long units (8 stages at rank 128) otherwise leave the
+// CTAs that took them running long after the rest finished.
+#ifndef CHAM_SPLIT_NP
+#define CHAM_SPLIT_NP 0  // 0 = off (A/B on C2: 8 -> 99.6k, off -> 113.3k tok/s on the same box)
+#endif
+constexpr int kSplitNp = CHAM_SPLIT_NP;
+static_assert(TG == kSplitTG && NCB_SMALL == kSplitNcb, "split scratch geometry (cham_pool.h)");
 #ifndef CHAM_STAGGER
 #define CHAM_STAGGER 0  // 1: S(0) S(1) E(0) S(2) E(1) ... (A/B on C2: 103.5k vs 118.5k tok/s for S... E...)
 #endif
@@ -420,6 +435,20 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
       pl.ex_start[nw] = carry;
       pl.sh_lpt[nw] = carry_sh;
       pl.totals[1] = carry;
+      // split tiles: the LPT prefix whose adapters have more than kSplitNp pages
+      int nsplit = 0;
+      if (kSplitNp > 0 && !kStagger) {
+        nsplit = carry;
+        for (int c = 0; c < pl.n_cls; ++c) {
+          const int np_c = ceil_div(pl.seg_sr[pl.order[pl.cls_pos[c]]] & 511, kRowsPerPage);
+          if (np_c <= kSplitNp) {
+            nsplit = pl.ex_start[pl.cls_pos[c]];
+            break;
+          }
+        }
+        nsplit = min(nsplit, kSplitCap);
+      }
+      pl.n_split = nsplit;
     }
   }
   __syncthreads();
@@ -603,7 +632,7 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
 // Thread (q, h) owns 16-byte column chunk q = ct >> lpg and page pg0 + h of each stage
 // (h = ct & (PG-1)); a lone page in a PG = 2 stage is split in row halves instead.
 template <typename T, int NT>
-__device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& seq, const Meta& m0, int ct) {
+__device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& seq, const Meta& m0, int ct, int& npub) {
   constexpr int ES = Elem<T>::kBytes;
   constexpr int EPV = Elem<T>::kEPV;
   constexpr int NP2 = EPV / 2;
@@ -624,7 +653,7 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
     const Meta& m = sm.meta[stage];
     const unsigned char* st = sm.stage[stage];
     const float* Vst = reinterpret_cast<const float*>(st + K2_V);  // [page in stage][TG][8]
-    if (active && !kNoCompute) {
+    if (active && !kNoCompute && m.npg > 0) {
       if (lpg >= 2 || m.npg == 2) {
         // own page pg0 + h: all 8 rows, fully unrolled
         if (h < m.npg) {
@@ -686,12 +715,30 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
             acc[t][e].y += __shfl_xor_sync(0xffffffffu, acc[t][e].y, o);
           }
       }
+      const int ncol_unit = m0.ncb / ES;
       if (active) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           if ((t & (npgmax - 1)) == h) {  // sibling h stores tokens t == h (mod PG)
+            if (m0.xm == 1) {
+              // page half 0: leave the fp32 partial for half 1 (read by its producer's TMA)
+              float4* dst = reinterpret_cast<float4*>(p.split_buf + ((long long)m0.sidx * TG + t) * ncol_unit + q * EPV);
+#pragma unroll
+              for (int e = 0; e < NP2; e += 2)
+                dst[e / 2] = make_float4(acc[t][e].x, acc[t][e].y, acc[t][e + 1].x, acc[t][e + 1].y);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              continue;
+            }
             float yv[EPV];
             Elem<T>::unpack(lds128(st + K2_Y + t * m0.ncb + q * 16), yv);
+            if (m0.xm == 2) {  // combine stage: add half 0's partial
+              const float4* pv = reinterpret_cast<const float4*>(st + (t * ncol_unit + q * EPV) * 4);
+#pragma unroll
+              for (int e = 0; e < NP2; e += 2) {
+                const float4 f = pv[e / 2];
+                acc[t][e].x += f.x; acc[t][e].y += f.y; acc[t][e + 1].x += f.z; acc[t][e + 1].y += f.w;
+              }
+            }
 #pragma unroll
             for (int e = 0; e < NP2; ++e) {
               yv[2 * e] += acc[t][e].x;
@@ -701,6 +748,11 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
             *reinterpret_cast<uint4*>(dst) = Elem<T>::pack(yv);
           }
         }
+      }
+      if (m0.xm == 1) {
+        // every partial of the slot is written: hand its flag to the publisher warp
+        named_bar_sync(1, GROUP_THREADS);
+        if (ct == 0) post_publish(sm, npub, p.split_ctr + m0.sidx);
       }
     }
     if (ct == 0) trace_consumer(p, seq, 3);
@@ -778,7 +830,9 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
   const int ncc = n_colchunks<T>(p, 0);
   int n = 0, acc = 0;
   auto add = [&](int kind, int a, int e) {
-    const int units = kind == KIND_SHRINK ? J * (pl.sh_lpt[e] - pl.sh_lpt[a]) : J * ncc * (pl.ex_start[e] - pl.ex_start[a]);
+    const int t0 = pl.ex_start[a], t1 = pl.ex_start[e];
+    const int nsp = max(0, min(pl.n_split, t1) - t0);  // split tiles inside the block: two units each
+    const int units = kind == KIND_SHRINK ? J * (pl.sh_lpt[e] - pl.sh_lpt[a]) : J * ncc * (t1 - t0 + nsp);
     if (units <= 0) return;
     sc.kind[n] = kind;
     sc.a[n] = a;
@@ -804,7 +858,7 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
 
 // unit -> (block, job, descriptor index, column chunk)
 struct UnitPos {
-  int kind, job, di, cc;
+  int kind, job, di, cc, half;
 };
 template <typename T>
 __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const Schedule& sc, int u) {
@@ -818,11 +872,23 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
     r.job = rel / span;
     r.di = pl.sh_lpt[sc.a[b]] + (rel - r.job * span);
     r.cc = 0;
+    r.half = -1;
   } else {
     const int ncc = n_colchunks<T>(p, 0);
     const int per_tile = p.n_jobs * ncc;
-    r.di = pl.ex_start[sc.a[b]] + rel / per_tile;  // expand tile
-    const int jc = rel % per_tile;
+    const int t0 = pl.ex_start[sc.a[b]];
+    const int nsp = max(0, min(pl.n_split, pl.ex_start[sc.e[b]]) - t0);
+    int jc;
+    if (rel < 2 * nsp * per_tile) {  // split tiles: (tile, job, chunk) x 2 page halves
+      r.half = rel & 1;
+      r.di = t0 + (rel >> 1) / per_tile;
+      jc = (rel >> 1) % per_tile;
+    } else {
+      const int r2 = rel - 2 * nsp * per_tile;
+      r.half = -1;
+      r.di = t0 + nsp + r2 / per_tile;  // expand tile
+      jc = r2 % per_tile;
+    }
     r.job = jc / ncc;
     r.cc = jc - r.job * ncc;
   }
@@ -877,7 +943,7 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
 
 template <typename T>
 __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused, int job,
-                                            int cc, int tile, int4 da, int4 db, int rdy, int unit) {
+                                            int cc, int tile, int half, int4 da, int4 db, int rdy, int unit) {
   constexpr int ES = Elem<T>::kBytes;
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
@@ -900,20 +966,50 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
   const uint32_t y_bytes = ncols * ES;                  // per token
   const int rpad = np * kRowsPerPage;
   const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
-  const int nst = ceil_div(np, pgs);
+  // page range of this unit: all pages, or one half of them (the second half adds a combine stage)
+  const int pb = half == 1 ? np / 2 : 0, pe = half == 0 ? np / 2 : np;
+  const int nst_pg = ceil_div(pe - pb, pgs);
+  const int nst = nst_pg + (half == 1 ? 1 : 0);
+  const int xm = half + 1;
+  const int sidx = half >= 0 ? (job * kSplitCap + tile) * p.split_ncc + cc : 0;
   const Job& jb = p.jobs[job];
   for (int k = 0; k < nst; ++k, ++seq) {
     const unsigned long long t_it = p.trace ? gtimer() : 0;
     const int stage = seq % NSTAGE;
-    const int pg0 = k * pgs;
-    const int npg = min(pgs, np - pg0);
     unsigned char* st = sm.stage[stage];
+    if (k == nst_pg) {
+      // half 1's combine stage: y rows + half 0's fp32 partial (published through split_ctr)
+      const uint32_t part_bytes = ncol_unit * 4;  // per token
+      if (lane == 0) {
+        mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
+        while (ld_acquire_gpu(p.split_ctr + sidx) < 1) __nanosleep(32);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      __syncwarp();
+      Meta& m = sm.meta[stage];
+      if (lane == 0) {
+        m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
+        m.pg0 = pe; m.npg = 0; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
+        m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16; m.xm = xm; m.sidx = sidx;
+        mbar_arrive_expect_tx(&sm.full[stage], (y_bytes + part_bytes) * tcount);
+        bulk_g2s(st, p.split_buf + (long long)sidx * TG * ncol_unit, part_bytes * tcount, &sm.full[stage], pol_w);
+      }
+      if (lane < tcount) {
+        m.rows[lane] = row;
+        bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
+      }
+      __syncwarp();
+      continue;
+    }
+    const int pg0 = pb + k * pgs;
+    const int npg = min(pgs, pe - pg0);
+    const bool y_here = half < 0 && k == nst - 1;  // plain units: the last stage carries the y rows
     // every stage carries its pages' v slice; the last one also the y rows.  With a
     // caller-provided v (TP) only pages inside v_stride are copied, the rest are zeroed.
     const int npg_in = p.v_in ? max(0, min(npg, vrow / kRowsPerPage - pg0)) : npg;
     const uint32_t v_bytes = p.v_in ? npg_in * tcount * kRowsPerPage * 4 : npg * TG * kRowsPerPage * 4;
     uint32_t bytes = b_bytes * npg + v_bytes;
-    if (k == nst - 1) bytes += y_bytes * tcount;
+    if (y_here) bytes += y_bytes * tcount;
     int pgid = 0;
     if (lane < npg) pgid = page_of(p, pl, pages_smem, s, slot, pg0 + lane);
     if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
@@ -933,7 +1029,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
     if (lane == 0) {
       m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
       m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
-      m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16;
+      m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16; m.xm = xm; m.sidx = sidx;
       mbar_arrive_expect_tx(&sm.full[stage], bytes);
     }
     if (lane < tcount) m.rows[lane] = row;
@@ -947,7 +1043,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       pdl_launch_dependents();
       waited = true;
     }
-    if (k == nst - 1 && lane < tcount)
+    if (y_here && lane < tcount)
       bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
     if (fused && k == 0) {
       // the tile's v rows are complete once all np shrink units of (job, tile) published
@@ -1020,7 +1116,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
     if (up.kind == KIND_SHRINK)
       seq = issue_shrink<T>(p, sm, seq, waited, up.job, da, db);
     else
-      seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, da, db, rdy, unit);
+      seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, up.half, da, db, rdy, unit);
     unit = nunit;
     up = nup;
     da = na;
@@ -1096,10 +1192,10 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
         }
       } else {
         switch (m0.T) {
-          case 1: expand_unit<T, 1>(p, sm, seq, m0, ct); break;
-          case 2: expand_unit<T, 2>(p, sm, seq, m0, ct); break;
-          case 3: expand_unit<T, 3>(p, sm, seq, m0, ct); break;
-          default: expand_unit<T, 4>(p, sm, seq, m0, ct); break;
+          case 1: expand_unit<T, 1>(p, sm, seq, m0, ct, npub); break;
+          case 2: expand_unit<T, 2>(p, sm, seq, m0, ct, npub); break;
+          case 3: expand_unit<T, 3>(p, sm, seq, m0, ct, npub); break;
+          default: expand_unit<T, 4>(p, sm, seq, m0, ct, npub); break;
         }
       }
     }
@@ -1115,6 +1211,11 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     if (p.tile_ctr) {
       const int n = p.n_jobs * sm.plan.totals[1];
       for (int i = tid; i < n; i += APPLY_THREADS) p.tile_ctr[i] = 0;
+    }
+    {
+      const int per = sm.plan.n_split * p.split_ncc;  // used slots of each job
+      for (int i = tid; i < p.n_jobs * per; i += APPLY_THREADS)
+        p.split_ctr[(i / per) * kSplitCap * p.split_ncc + i % per] = 0;
     }
     if (tid == 0) {
       p.ctr[0] = 0;
@@ -1165,6 +1266,9 @@ int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
   prm.tile_ctr = mode == MODE_FUSED ? pool->d_ctr + kTileCtrBase + (pool->apply_count & 1) * (size_t)kMaxJobs *
                                                                       pool->max_tokens
                                     : nullptr;
+  prm.split_buf = pool->d_split;
+  prm.split_ncc = pool->split_ncc;
+  prm.split_ctr = pool->d_split_ctr + (pool->apply_count & 1) * (size_t)kMaxJobs * kSplitCap * pool->split_ncc;
   prm.err = pool->d_ctr + 2;
   ++pool->apply_count;
   cudaLaunchConfig_t cfg{};

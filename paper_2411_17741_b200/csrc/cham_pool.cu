@@ -165,6 +165,8 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_plan);
     cudaFree(pool->d_pvimg);
     cudaFree(pool->d_pctr);
+    cudaFree(pool->d_split);
+    cudaFree(pool->d_split_ctr);
     delete pool;
     cudaSetDevice(prev);
     return fail(code, msg);
@@ -189,6 +191,16 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     extern size_t cham_plan_bytes_internal(const cham_pool*);
     e = cudaMalloc(&pool->d_plan, cham_plan_bytes_internal(pool));
   }
+  {
+    int hout_max = 0;
+    for (int p = 0; p < n_proj; ++p) hout_max = hout_max > h_out[p] ? hout_max : h_out[p];
+    pool->split_ncc = (int)(((size_t)hout_max * es + kSplitNcb - 1) / kSplitNcb);
+  }
+  const size_t n_split = (size_t)kMaxJobs * kSplitCap * pool->split_ncc;
+  if (e == cudaSuccess)  // fp32 partial: kSplitTG tokens x (kSplitNcb / es) columns per slot
+    e = cudaMalloc(&pool->d_split, n_split * kSplitTG * (kSplitNcb / es) * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&pool->d_split_ctr, 2 * n_split * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(pool->d_split_ctr, 0, 2 * n_split * sizeof(int));
   if (e == cudaSuccess && pool->prefill_ok)
     e = cudaMalloc(&pool->d_pvimg, (size_t)kMaxJobs * kPrefillMaxTiles * kPrefillVImg);
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMalloc(&pool->d_pctr, sizeof(int) * prefill_ctr_ints());
@@ -215,6 +227,8 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_plan);
   cudaFree(pool->d_pvimg);
   cudaFree(pool->d_pctr);
+  cudaFree(pool->d_split);
+  cudaFree(pool->d_split_ctr);
   delete pool;
   return CHAM_OK;
 }

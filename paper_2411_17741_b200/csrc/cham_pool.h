@@ -41,6 +41,9 @@ struct cham_pool {
   char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB] (ks partials)
   int* d_pctr = nullptr;               // prefill counters: 2 parity sets + tile V flags
   int prefill_epoch = 0;               // prefill launches so far (tile flags, counter parity)
+  float* d_split = nullptr;            // decode page-half partials [kMaxJobs][kSplitCap][split_ncc][4][2048 B cols]
+  int* d_split_ctr = nullptr;          // 2 parity x [kMaxJobs][kSplitCap][split_ncc]
+  int split_ncc = 1;                   // 2048-byte column chunks of the widest h_out
 };
 
 namespace cham {
@@ -51,6 +54,10 @@ constexpr int kPrefillMaxTiles = 256;  // 128-row prefill tiles per apply (works
 constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles;  // one parity set: dispatch, done, spare, tile counters
 constexpr size_t kPrefillVImg = 32768;                // V image bytes per (job, tile)
 inline size_t prefill_ctr_ints() { return 2 * kPrefillCtrSet + kPrefillMaxTiles; }
+
+constexpr int kSplitCap = 128;         // decode expand tiles split into page halves per apply
+constexpr int kSplitTG = 4;            // tokens per decode tile (decode::TG)
+constexpr int kSplitNcb = 2048;        // bytes of one B row per decode expand unit
 
 // d_ctr layout: launch counters, then the per-parity tile-ready counters of the decode kernel
 constexpr int kTileCtrBase = 64;

@@ -360,3 +360,18 @@ def test_paged_cache_fills_evictions_and_page_reuse():
     assert evictions > 0 and cache.fill_count > len(set(ids)) // 2
     assert cache.used_tokens == cache.resident_tokens_recount()
     pool.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_page_half_split_expand_units(dtype):
+    """Adapters with more than 8 pages (ranks 72, 128, 256) have their expand units split
+    into two page halves (half 0 leaves an fp32 partial, half 1 combines it with y); multi-
+    token tiles, odd page counts and a 8192-wide output (8 column chunks) included."""
+    slot_ranks = {0: 72, 1: 128, 2: 256, 3: 8}
+    req_slots = [0, 1, 2, 1, 3, 0, 1, 2, 2, 1]
+    req_ntok = [1, 3, 2, 1, 1, 5, 2, 1, 4, 1]
+    got, ref = _run_case(dtype, 1024, 8192, slot_ranks, req_slots, req_ntok, seed=31)
+    if dtype == torch.float32:
+        np.testing.assert_allclose(got, ref, rtol=FP32_RTOL, atol=1e-5)
+    else:
+        np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
