@@ -187,6 +187,7 @@ def sim_batches(max_steps: int = 400):
             captured.append({
                 "prefills": [[r.spec.adapter_id, r.spec.input_tokens] for r in prefills],
                 "decoders": [r.spec.adapter_id for r in decoders],
+                "decoder_active": [r.spec.input_tokens + r.tokens_generated for r in decoders],
                 "adapter_units": units,
                 "duration_us": orig(self, prefills, decoders, rank_of),
             })

@@ -843,11 +843,13 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
   };
   const int C = pl.n_cls;
   if (kStagger) {
+    // E(c) follows S(c + kStagger): the classes between give S(c) time to complete
     for (int c = 0; c < C; ++c) {
       if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[c], pl.cls_pos[c + 1]);
-      if (mode != MODE_SHRINK && c >= 1) add(KIND_EXPAND, pl.cls_pos[c - 1], pl.cls_pos[c]);
+      if (mode != MODE_SHRINK && c >= CHAM_STAGGER) add(KIND_EXPAND, pl.cls_pos[c - CHAM_STAGGER], pl.cls_pos[c - CHAM_STAGGER + 1]);
     }
-    if (mode != MODE_SHRINK && C >= 1) add(KIND_EXPAND, pl.cls_pos[C - 1], pl.cls_pos[C]);
+    if (mode != MODE_SHRINK)
+      for (int c = max(0, C - CHAM_STAGGER); c < C; ++c) add(KIND_EXPAND, pl.cls_pos[c], pl.cls_pos[c + 1]);
   } else {
     if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[0], pl.cls_pos[C]);
     if (mode != MODE_SHRINK) add(KIND_EXPAND, pl.cls_pos[0], pl.cls_pos[C]);

@@ -155,8 +155,8 @@ class LoraStepExecutor:
 
     def launches_per_step(self) -> int:
         """Kernels per step: segment builder + plan + per (layer, group) the decode kernel
-        and/or the two tcgen05 prefill kernels."""
-        per = (1 if self.decode_launched else 0) + (2 if self.prefill_launched else 0)
+        and/or the fused tcgen05 prefill kernel."""
+        per = (1 if self.decode_launched else 0) + (1 if self.prefill_launched else 0)
         return 2 + self.pool.n_layers * len(self.proj_groups) * per
 
     def run(self, xs_per_layer, ys_per_layer, stream=None) -> None:

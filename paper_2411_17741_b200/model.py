@@ -94,3 +94,16 @@ def zipf_catalog(num_adapters: int, rank_set=DEFAULT_RANK_SET, s: float = 0.7):
         ids.append(f"r{rank}-{i // len(ranks)}")
         probs.append(raw[i] / z)
     return ids, probs
+
+
+@dataclass
+class CostModelParams:
+    """The reference's linear iteration-time coefficients (model.py:159-172), in microseconds;
+    the adapter term is per (rank x token processed).  B200CostModel (cost_model.py) keeps the
+    base-model terms and replaces the adapter term with a measured latency model."""
+
+    prefill_base_us: float = 5_000.0
+    prefill_per_token_us: float = 40.0
+    decode_base_us: float = 6_000.0
+    decode_per_token_us: float = 25.0
+    adapter_compute_per_rank_token_us: float = 0.155
