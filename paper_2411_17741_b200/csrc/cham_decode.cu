@@ -211,6 +211,13 @@ constexpr int MAX_BLOCKS = 2 * (kMaxPagesPerSlot + 1);
 #define CHAM_SPLIT_NP 0  // 0 = off (A/B on C2: 8 -> 99.6k, off -> 113.3k tok/s on the same box)
 #endif
 constexpr int kSplitNp = CHAM_SPLIT_NP;
+// Alternative for the large-rank tiles (np > 8): the tier-2 expand geometry (8 pages x 256
+// columns per stage, 2-stage units, 16 column chunks per tile) instead of the page halves.
+// 2: on (A/B on C2: 101.1k vs 114.6k tok/s off), 0: off.
+#ifndef CHAM_BIG_TIER
+#define CHAM_BIG_TIER 0
+#endif
+constexpr int kBigTier = CHAM_BIG_TIER;
 static_assert(TG == kSplitTG && NCB_SMALL == kSplitNcb, "split scratch geometry (cham_pool.h)");
 #ifndef CHAM_STAGGER
 #define CHAM_STAGGER 0  // 1: S(0) S(1) E(0) S(2) E(1) ... (A/B on C2: 103.5k vs 118.5k tok/s for S... E...)
@@ -437,11 +444,11 @@ __device__ bool build_plan(const Params& p, Plan& pl, int S, UnitDesc* desc = nu
       pl.totals[1] = carry;
       // split tiles: the LPT prefix whose adapters have more than kSplitNp pages
       int nsplit = 0;
-      if (kSplitNp > 0 && !kStagger) {
+      if ((kSplitNp > 0 || kBigTier > 0) && !kStagger) {
         nsplit = carry;
         for (int c = 0; c < pl.n_cls; ++c) {
           const int np_c = ceil_div(pl.seg_sr[pl.order[pl.cls_pos[c]]] & 511, kRowsPerPage);
-          if (np_c <= kSplitNp) {
+          if (np_c <= (kSplitNp > 0 ? kSplitNp : 8)) {
             nsplit = pl.ex_start[pl.cls_pos[c]];
             break;
           }
@@ -831,8 +838,13 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
   int n = 0, acc = 0;
   auto add = [&](int kind, int a, int e) {
     const int t0 = pl.ex_start[a], t1 = pl.ex_start[e];
-    const int nsp = max(0, min(pl.n_split, t1) - t0);  // split tiles inside the block: two units each
-    const int units = kind == KIND_SHRINK ? J * (pl.sh_lpt[e] - pl.sh_lpt[a]) : J * ncc * (t1 - t0 + nsp);
+    const int nsp = max(0, min(pl.n_split, t1) - t0);  // split tiles inside the block
+    const bool big_tier = kBigTier == 2;
+    const int ncc2 = n_colchunks<T>(p, 2);
+    const int units = kind == KIND_SHRINK ? J * (pl.sh_lpt[e] - pl.sh_lpt[a])
+                      : big_tier          ? J * (ncc * (t1 - t0 - nsp) + ncc2 * nsp)
+                      : kSplitNp > 0      ? J * ncc * (t1 - t0 + nsp)
+                                          : J * ncc * (t1 - t0);
     if (units <= 0) return;
     sc.kind[n] = kind;
     sc.a[n] = a;
@@ -860,7 +872,7 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
 
 // unit -> (block, job, descriptor index, column chunk)
 struct UnitPos {
-  int kind, job, di, cc, half;
+  int kind, job, di, cc, half, tier;
 };
 template <typename T>
 __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const Schedule& sc, int u) {
@@ -875,13 +887,30 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
     r.di = pl.sh_lpt[sc.a[b]] + (rel - r.job * span);
     r.cc = 0;
     r.half = -1;
+    r.tier = 0;
   } else {
     const int ncc = n_colchunks<T>(p, 0);
     const int per_tile = p.n_jobs * ncc;
     const int t0 = pl.ex_start[sc.a[b]];
     const int nsp = max(0, min(pl.n_split, pl.ex_start[sc.e[b]]) - t0);
+    const bool big_tier = kBigTier == 2;
     int jc;
-    if (rel < 2 * nsp * per_tile) {  // split tiles: (tile, job, chunk) x 2 page halves
+    r.tier = 0;
+    if (big_tier && rel < nsp * p.n_jobs * n_colchunks<T>(p, 2)) {  // large-rank tiles, tier-2 geometry
+      const int ncc2 = n_colchunks<T>(p, 2), per2 = p.n_jobs * ncc2;
+      r.half = -1;
+      r.tier = 2;
+      r.di = t0 + rel / per2;
+      jc = rel % per2;
+      r.job = jc / ncc2;
+      r.cc = jc - r.job * ncc2;
+      return r;
+    } else if (big_tier) {
+      const int r2 = rel - nsp * p.n_jobs * n_colchunks<T>(p, 2);
+      r.half = -1;
+      r.di = t0 + nsp + r2 / per_tile;
+      jc = r2 % per_tile;
+    } else if (kSplitNp > 0 && rel < 2 * nsp * per_tile) {  // split tiles: (tile, job, chunk) x 2 page halves
       r.half = rel & 1;
       r.di = t0 + (rel >> 1) / per_tile;
       jc = (rel >> 1) % per_tile;
@@ -945,7 +974,8 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
 
 template <typename T>
 __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused, int job,
-                                            int cc, int tile, int half, int4 da, int4 db, int rdy, int unit) {
+                                            int cc, int tile, int half, int tier, int4 da, int4 db, int rdy,
+                                            int unit) {
   constexpr int ES = Elem<T>::kBytes;
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
@@ -957,10 +987,12 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
   const int vbase = da.w;
   const int row = lane == 0 ? db.x : lane == 1 ? db.y : lane == 2 ? db.z : db.w;
   const int slot = pl.seg_sr[s] >> 9;
-  const int lpg = 1;           // two consumer threads per 16-byte column chunk
-  const int pgs = EX_PAGES;    // one page per stage: the two threads split its rows
-  const int ncb = tier_ncb(0);
-  const int pitch = tier_pitch(0);
+  // tier 0: two consumer threads per 16-byte column chunk (EX_PAGES pages per stage; one page
+  // is split in row halves); tier 2: eight threads, one page each, 8 pages per stage
+  const int lpg = tier == 2 ? 3 : 1;
+  const int pgs = tier == 2 ? 8 : EX_PAGES;
+  const int ncb = tier_ncb(tier);
+  const int pitch = tier_pitch(tier);
   const int ncol_unit = ncb / ES;
   const int col0 = cc * ncol_unit;
   const int ncols = min(ncol_unit, p.h_out - col0);
@@ -1118,7 +1150,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
     if (up.kind == KIND_SHRINK)
       seq = issue_shrink<T>(p, sm, seq, waited, up.job, da, db);
     else
-      seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, up.half, da, db, rdy, unit);
+      seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit);
     unit = nunit;
     up = nup;
     da = na;

@@ -39,7 +39,7 @@ def setup(n_layers=L):
         buf = (torch.randn(npg * pool.page_bytes // 2, device=dev) * 0.02).to(torch.bfloat16)
         pool.fill_from_device(slot_of[a], buf.view(torch.uint8))
         page += npg
-    batch = decode_batch(0)
+    batch = decode_batch(0, int(os.environ.get("TRACE_T", "256")))
     req_slot = [slot_of[a] for a in batch]
     req_rank = [rank_of_id(a) for a in batch]
     return pool, req_slot, req_rank

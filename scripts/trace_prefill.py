@@ -4,6 +4,7 @@ Per launch (q/k/v fused, then o): per unit kind the loader issue span, MMA span 
 span, the epilogue lag behind the loader, and per-CTA start/finish spread.  Saves the raw
 trace to gpurun_out/trace_prefill_<name>.npy.
 """
+import os
 import sys
 from pathlib import Path
 
@@ -24,6 +25,8 @@ H, L, P = 4096, 2, 4
 def main():
     dev = torch.device("cuda", 0)
     pids, pntok = prefill_batch(0)
+    nseg = int(os.environ.get("TRACE_NSEG", "64"))
+    pids, pntok = pids[:nseg], pntok[:nseg]
     ids = list(dict.fromkeys(pids))
     rank_of = {a: rank_of_id(a) for a in ids}
     slot_of = {a: i for i, a in enumerate(ids)}
