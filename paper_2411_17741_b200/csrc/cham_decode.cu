@@ -223,6 +223,9 @@ static_assert(TG == kSplitTG && NCB_SMALL == kSplitNcb, "split scratch geometry 
 #define CHAM_STAGGER 0  // 1: S(0) S(1) E(0) S(2) E(1) ... (A/B on C2: 103.5k vs 118.5k tok/s for S... E...)
 #endif
 constexpr bool kStagger = CHAM_STAGGER != 0;
+#ifndef CHAM_STAGGER_1JOB
+#define CHAM_STAGGER_1JOB 0  // stagger gap for single-projection launches only
+#endif
 struct Schedule {
   int n;
   int start[MAX_BLOCKS + 1];  // unit prefix
@@ -854,14 +857,15 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
     ++n;
   };
   const int C = pl.n_cls;
-  if (kStagger) {
-    // E(c) follows S(c + kStagger): the classes between give S(c) time to complete
+  const int gap = kStagger ? CHAM_STAGGER : (J == 1 ? CHAM_STAGGER_1JOB : 0);
+  if (gap > 0) {
+    // E(c) follows S(c + gap): the classes between give S(c) time to complete
     for (int c = 0; c < C; ++c) {
       if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[c], pl.cls_pos[c + 1]);
-      if (mode != MODE_SHRINK && c >= CHAM_STAGGER) add(KIND_EXPAND, pl.cls_pos[c - CHAM_STAGGER], pl.cls_pos[c - CHAM_STAGGER + 1]);
+      if (mode != MODE_SHRINK && c >= gap) add(KIND_EXPAND, pl.cls_pos[c - gap], pl.cls_pos[c - gap + 1]);
     }
     if (mode != MODE_SHRINK)
-      for (int c = max(0, C - CHAM_STAGGER); c < C; ++c) add(KIND_EXPAND, pl.cls_pos[c], pl.cls_pos[c + 1]);
+      for (int c = max(0, C - gap); c < C; ++c) add(KIND_EXPAND, pl.cls_pos[c], pl.cls_pos[c + 1]);
   } else {
     if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[0], pl.cls_pos[C]);
     if (mode != MODE_SHRINK) add(KIND_EXPAND, pl.cls_pos[0], pl.cls_pos[C]);
