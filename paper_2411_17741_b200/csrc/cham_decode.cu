@@ -41,6 +41,14 @@ namespace decode {
 #define CHAM_EXP_NOCOMPUTE 0  // experiment builds only: consumers skip the math (data-movement ceiling)
 #endif
 constexpr bool kNoCompute = CHAM_EXP_NOCOMPUTE != 0;
+#ifndef CHAM_MMA_SHRINK
+#define CHAM_MMA_SHRINK 0  // 1: bf16 shrink on mma.sync (A/B on C2: 99.4k vs 114.9k tok/s FFMA2)
+#endif
+constexpr bool kMmaShrink = CHAM_MMA_SHRINK != 0;
+#ifndef CHAM_MMA_EXPAND
+#define CHAM_MMA_EXPAND 0  // 1: bf16 expand on mma.sync (A/B on C2: 104.0k vs 114.9k tok/s FFMA2)
+#endif
+constexpr bool kMmaExpand = CHAM_MMA_EXPAND != 0;
 
 constexpr int TG = 4;                        // tokens per tile
 #ifndef CHAM_NSTAGE
@@ -57,7 +65,8 @@ constexpr int A_CHUNK = CHAM_ACHUNK;         // K1: adapter bytes per stage (8 r
 constexpr int X_ROW = A_CHUNK / kRowsPerPage;  // K1: x bytes per token per stage (k-chunk)
 constexpr int EX_PAGES = CHAM_EXPG;          // K2: adapter pages per stage (1 or 2)
 static_assert(X_ROW <= kActRowBytes && (EX_PAGES == 1 || EX_PAGES == 2), "stage geometry");
-constexpr int K1_STAGE = A_CHUNK + TG * X_ROW;
+constexpr int X_PITCH = X_ROW + 16;         // staged x rows: +16 B so ldmatrix rows hit distinct banks
+constexpr int K1_STAGE = A_CHUNK + TG * X_PITCH;
 // K2 geometry tiers, chosen by the adapter's page count np so that every expand unit is at
 // most two 32 KiB stages (uniform units keep the dynamic dispatch balanced to the end —
 // with unit sizes from 16 to 256 KiB, large units claimed late by the look-ahead dispatch
@@ -560,6 +569,109 @@ __device__ __forceinline__ void post_publish(Shared& sm, int& npub, int* ctr) {
   mbar_arrive(&sm.pub_full[slot]);
 }
 
+// ---------------------------------------------------------------- K1 on the tensor cores (bf16)
+// The shrink of a 4-token tile against one page is a [T x K] . [K x 8] product: each consumer
+// warp runs mma.sync m16n8k16 (bf16 in, fp32 accumulate) over its 1/8 of the stage's K range,
+// x rows as the A operand (tokens padded to 16: rows >= T repeat row 0 and are discarded) and
+// the page's A^T rows (already K-major and 128 B-swizzled) as the B operand via ldmatrix; the
+// eight warp partials are summed through shared memory at the end of the unit.
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t (&r)[2]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+__device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <int NT>
+__device__ __forceinline__ void shrink_unit_mma(const Params& p, const Plan& pl, K1Shared& sm, int& seq,
+                                                const Meta& m0, float* red, int ct, int lane, int gw, int& npub) {
+  constexpr int ES = 2;
+  constexpr int NACC = 4;  // independent accumulators: consecutive k-steps do not wait on each other
+  float dd[NACC][4];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) dd[i][0] = dd[i][1] = dd[i][2] = dd[i][3] = 0.f;
+  // ldmatrix row addresses: x (A operand) row rr = lane % 8 + 8 * ((lane / 8) & 1), k half lane / 16;
+  // A^T (B operand) rank row j = lane % 8, k half (lane / 8) & 1
+  const int rr = (lane & 7) + 8 * ((lane >> 3) & 1);
+  const int xrow = rr < NT ? rr : 0;
+  const int xko = (lane >> 4) * 8;
+  const int bj = lane & 7, bko = ((lane >> 3) & 1) * 8;
+  for (int k = 0; k < m0.nst; ++k, ++seq) {
+    const int stage = seq % NSTAGE;
+    if (k > 0) mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
+    if (ct == 0) trace_consumer(p, seq, 2);
+    const Meta& m = sm.meta[stage];
+    const unsigned char* st = sm.stage[stage];
+    const int kel = min(X_ROW, p.h_in * ES - m.kc * X_ROW) / ES;  // K elements in this stage
+    const int per_warp = kel / GROUP_WARPS;                        // multiple of 16 (h_in % 128 == 0)
+    const uint32_t xbase = smem_u32(st + A_CHUNK + xrow * X_PITCH) + xko * ES;
+    const uint32_t abase = smem_u32(st);
+    if (!kNoCompute) {
+      for (int k0 = gw * per_warp; k0 < (gw + 1) * per_warp; k0 += 16 * NACC) {
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) {
+          const int kk = k0 + i * 16;
+          if (kk < (gw + 1) * per_warp) {
+            uint32_t a[4], b[2];
+            ldsm_x4(xbase + kk * ES, a);
+            const int kb = kk + bko;  // this lane's 8-element K chunk of the B rows
+            ldsm_x2(abase + (kb >> 6) * kAtomBytes + bj * kRowBytes + ((((kb >> 3) & 7) ^ bj) << 4), b);
+            mma_16816(dd[i], a, b);
+          }
+        }
+      }
+    }
+    if (ct == 0) trace_consumer(p, seq, 3);
+    mbar_arrive(&sm.empty[stage]);  // this stage has been read: hand it back
+  }
+  // C fragment: d[0], d[1] = (token row lane / 4, rank rows 2 (lane % 4), +1); rows >= NT are padding
+  float d[2] = {0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) {
+    d[0] += dd[i][0];
+    d[1] += dd[i][1];
+  }
+  named_bar_sync(1, GROUP_THREADS);  // the previous unit's readers of `red` are done
+  const int g = lane >> 2, c2 = (lane & 3) * 2;
+  if (g < NT) {
+    red[(gw * TG + g) * kRowsPerPage + c2] = d[0];
+    red[(gw * TG + g) * kRowsPerPage + c2 + 1] = d[1];
+  }
+  named_bar_sync(1, GROUP_THREADS);
+  if (ct < NT * kRowsPerPage) {
+    const int t = ct / kRowsPerPage, j = ct % kRowsPerPage;
+    float sum = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < GROUP_WARPS; ++w2) sum += red[(w2 * TG + t) * kRowsPerPage + j];
+    const int row = m0.g * kRowsPerPage + j;
+    if (p.v_out) {
+      if (row < p.v_stride) p.v_out[(long long)(m0.pos0 + t) * p.v_stride + row] = sum;  // TP [position][v_stride]
+    } else {
+      const int tile = (m0.pos0 - pl.seg_off[m0.seg]) / TG;
+      const long long vb = pl.v_start[m0.seg] + (long long)tile * TG * m0.np * kRowsPerPage;
+      p.vws[m0.job * p.vws_job_stride + vb + (m0.g * TG + t) * kRowsPerPage + j] = sum;
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // read later by TMA (async proxy)
+    }
+  }
+  if (p.tile_ctr && gw == 0) {
+    // this page's v rows of the tile are final: hand the tile counter to the publisher warp
+    __syncwarp();
+    if (lane == 0) {
+      const int tile = pl.ex_start[pl.order_pos[m0.seg]] + (m0.pos0 - pl.seg_off[m0.seg]) / TG;
+      post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile);
+    }
+  }
+}
+
 template <typename T, int NT>
 __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1Shared& sm, int& seq, const Meta& m0,
                                             float* red, int ct, int lane, int gw, int& npub) {
@@ -585,7 +697,7 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
       const int a = q >> 3, c = q & 7;
       float2 xf[NT][NP2];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) Elem<T>::unpack2(lds128(X + t * X_ROW + q * 16), xf[t]);
+      for (int t = 0; t < NT; ++t) Elem<T>::unpack2(lds128(X + t * X_PITCH + q * 16), xf[t]);
 #pragma unroll
       for (int j = 0; j < kRowsPerPage; ++j) {
         float2 af[NP2];
@@ -634,6 +746,70 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
       const int tile = pl.ex_start[pl.order_pos[m0.seg]] + (m0.pos0 - pl.seg_off[m0.seg]) / TG;
       post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile);
     }
+  }
+}
+
+// ---------------------------------------------------------------- K2 on the tensor cores (bf16)
+// Y[T x 1024] += V[T x 16] . B[16 x 1024] per stage of two pages: each consumer warp owns 128
+// columns = 16 mma.sync m16n8k16 tiles; V (fp32 in the stage) is rounded to bf16 into the A
+// fragment (tokens padded to 16 rows, a lone page's missing 8 K rows zeroed), B comes straight
+// from the page layout (8 rank rows x 64 columns per swizzled atom) with ldmatrix.trans.
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t addr, uint32_t (&r)[2]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+
+template <int NT>
+__device__ __forceinline__ void expand_unit_mma(const Params& p, Shared& sm, int& seq, const Meta& m0, int ct,
+                                                int lane, int gw) {
+  constexpr int NTILE = (NCB_SMALL / 2) / 8 / GROUP_WARPS;  // 16 n-tiles of 8 columns per warp
+  float d[NTILE][4];
+#pragma unroll
+  for (int i = 0; i < NTILE; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.f;
+  const int g = lane >> 2, c2 = (lane & 3) * 2;
+  const int bj = lane & 7, bpg = (lane >> 3) & 1;  // ldmatrix row: rank row j of page bpg
+  const int wcol = gw * NTILE * 8;                  // this warp's first column in the unit
+  for (int k = 0; k < m0.nst; ++k, ++seq) {
+    const int stage = seq % NSTAGE;
+    if (k > 0) mbar_wait(&sm.full[stage], (seq / NSTAGE) & 1);
+    if (ct == 0) trace_consumer(p, seq, 2);
+    const Meta& m = sm.meta[stage];
+    const unsigned char* st = sm.stage[stage];
+    if (!kNoCompute) {
+      const float* Vst = reinterpret_cast<const float*>(st + K2_V);  // [page in stage][TG][8]
+      uint32_t a[4] = {0u, 0u, 0u, 0u};
+      if (g < NT) {
+        a[0] = pack_bf16x2(Vst[(0 * TG + g) * kRowsPerPage + c2], Vst[(0 * TG + g) * kRowsPerPage + c2 + 1]);
+        if (m.npg == 2)
+          a[2] = pack_bf16x2(Vst[(1 * TG + g) * kRowsPerPage + c2], Vst[(1 * TG + g) * kRowsPerPage + c2 + 1]);
+      }
+      // a lone page: its B rows stand in for the missing page (finite; multiplied by zero)
+      const uint32_t bbase = smem_u32(st + (m.npg == 2 ? bpg : 0) * m0.pitch) + bj * kRowBytes;
+#pragma unroll
+      for (int i = 0; i < NTILE; ++i) {
+        const int n0 = wcol + i * 8;
+        if (n0 * 2 < m0.ncols * 2) {
+          uint32_t b[2];
+          const int at = n0 >> 6, c = (n0 >> 3) & 7;
+          ldsm_x2_trans(bbase + at * kAtomBytes + (((c ^ bj) & 7) << 4), b);
+          mma_16816(d[i], a, b);
+        }
+      }
+    }
+    if (k == m0.nst - 1 && g < NT) {
+      // epilogue: y rows (staged bf16 in this stage) += D, stored straight to global
+      const unsigned char* yst = st + K2_Y + g * m0.ncb;
+      char* ydst = p.jobs[m0.job].y + ((long long)m0.rows[g] * p.h_out + m0.col0) * 2;
+#pragma unroll
+      for (int i = 0; i < NTILE; ++i) {
+        const int col = wcol + i * 8 + c2;
+        if (col < m0.ncols) {
+          const uint32_t yv = *reinterpret_cast<const uint32_t*>(yst + col * 2);
+          *reinterpret_cast<uint32_t*>(ydst + col * 2) = pack_bf16x2(bf_lo(yv) + d[i][0], bf_hi(yv) + d[i][1]);
+        }
+      }
+    }
+    if (ct == 0) trace_consumer(p, seq, 3);
+    mbar_arrive(&sm.empty[stage]);
   }
 }
 
@@ -968,7 +1144,7 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
       waited = true;
     }
     if (lane < tcount)
-      bulk_g2s(st + A_CHUNK + lane * X_ROW, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
+      bulk_g2s(st + A_CHUNK + lane * X_PITCH, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
                &sm.full[stage], pol_x);
     if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
     __syncwarp();
@@ -1223,17 +1399,41 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
       }
       if (m0.kind == KIND_SHRINK) {
         switch (m0.T) {
-          case 1: shrink_unit<T, 1>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
-          case 2: shrink_unit<T, 2>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
-          case 3: shrink_unit<T, 3>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
-          default: shrink_unit<T, 4>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub); break;
+          case 1:
+            if (kMmaShrink && Elem<T>::kDtype == CHAM_BF16 && p.h_in % 128 == 0) shrink_unit_mma<1>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            else shrink_unit<T, 1>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            break;
+          case 2:
+            if (kMmaShrink && Elem<T>::kDtype == CHAM_BF16 && p.h_in % 128 == 0) shrink_unit_mma<2>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            else shrink_unit<T, 2>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            break;
+          case 3:
+            if (kMmaShrink && Elem<T>::kDtype == CHAM_BF16 && p.h_in % 128 == 0) shrink_unit_mma<3>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            else shrink_unit<T, 3>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            break;
+          default:
+            if (kMmaShrink && Elem<T>::kDtype == CHAM_BF16 && p.h_in % 128 == 0) shrink_unit_mma<4>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            else shrink_unit<T, 4>(p, sm.plan, sm, seq, m0, red, ct, lane, gw, npub);
+            break;
         }
       } else {
         switch (m0.T) {
-          case 1: expand_unit<T, 1>(p, sm, seq, m0, ct, npub); break;
-          case 2: expand_unit<T, 2>(p, sm, seq, m0, ct, npub); break;
-          case 3: expand_unit<T, 3>(p, sm, seq, m0, ct, npub); break;
-          default: expand_unit<T, 4>(p, sm, seq, m0, ct, npub); break;
+          case 1:
+            if (kMmaExpand && Elem<T>::kDtype == CHAM_BF16 && m0.xm == 0 && m0.lpg == 1) expand_unit_mma<1>(p, sm, seq, m0, ct, lane, gw);
+            else expand_unit<T, 1>(p, sm, seq, m0, ct, npub);
+            break;
+          case 2:
+            if (kMmaExpand && Elem<T>::kDtype == CHAM_BF16 && m0.xm == 0 && m0.lpg == 1) expand_unit_mma<2>(p, sm, seq, m0, ct, lane, gw);
+            else expand_unit<T, 2>(p, sm, seq, m0, ct, npub);
+            break;
+          case 3:
+            if (kMmaExpand && Elem<T>::kDtype == CHAM_BF16 && m0.xm == 0 && m0.lpg == 1) expand_unit_mma<3>(p, sm, seq, m0, ct, lane, gw);
+            else expand_unit<T, 3>(p, sm, seq, m0, ct, npub);
+            break;
+          default:
+            if (kMmaExpand && Elem<T>::kDtype == CHAM_BF16 && m0.xm == 0 && m0.lpg == 1) expand_unit_mma<4>(p, sm, seq, m0, ct, lane, gw);
+            else expand_unit<T, 4>(p, sm, seq, m0, ct, npub);
+            break;
         }
       }
     }

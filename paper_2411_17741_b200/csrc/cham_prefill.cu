@@ -143,6 +143,34 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// two 32-column loads, one wait
+__device__ __forceinline__ void tmem_ld32x2(uint32_t taddr, float (&v0)[32], float (&v1)[32]) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr + 32));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    v0[i] = __uint_as_float(r[i]);
+    v1[i] = __uint_as_float(r[32 + i]);
+  }
+}
 // 2-D TMA tensor load (box defined by the map) completing on an mbarrier
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
                                             uint64_t policy) {
@@ -389,6 +417,10 @@ __device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileLis
 #define CHAM_WARM_L2 0  // A/B on C3: 461.7k (on) vs 520.8k tok/s (off)
 #endif
 constexpr bool kWarmL2 = CHAM_WARM_L2 != 0;
+#ifndef CHAM_EXP_NOEPI
+#define CHAM_EXP_NOEPI 0  // experiment builds only: the expand epilogue skips the y update
+#endif
+constexpr bool kNoEpi = CHAM_EXP_NOEPI != 0;
 // Warm L2 with a unit's operands as long contiguous runs (one x/y row range per token, one
 // run of atoms per adapter page): the TMA box loads then move 128-byte row pieces out of L2
 // instead of scattering 128-byte requests over DRAM pages.
@@ -909,13 +941,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           tc_fence_after();
           float d0[32], d1[32];
           const uint32_t ta = tmem + TM_EX + acc * 64 + lane_off;
-          tmem_ld32(ta, d0);
-          tmem_ld32(ta + 32, d1);
+          tmem_ld32x2(ta, d0, d1);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.tempty_ex[acc]);
           const int col0 = u.col0 + (s * u.kpc + g) * 64;
           unsigned char* yg = const_cast<unsigned char*>(ybase) + g * u.xb;
+          if (kNoEpi) continue;  // experiment builds: data-movement ceiling without the y update
           if (valid) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
