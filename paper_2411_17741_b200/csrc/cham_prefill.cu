@@ -780,6 +780,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         const int ab = nsh & 1;
         if (nsh >= 2) mbar_wait(&sm.tempty_sh[ab], ((nsh >> 1) - 1) & 1);
         tc_fence_after();
+        // (one MMA of N = jps * rp for the whole group would read x once per K step, but it
+        // faulted intermittently in long PDL chains: one MMA per job)
         const uint32_t idesc = idesc_bf16(BM, u.rp, false);
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
