@@ -192,7 +192,7 @@ def run_ours(args, rank: int, world: int):
     from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
     from paper_2411_17741_b200.workload import decode_batch, prefill_batch, rank_of_id
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     if args.config == "c3":
         # C3: 64 prefill segments x 64 tokens, one distinct adapter each (prefill_batch(seed=rank))
@@ -256,7 +256,7 @@ def run_ours(args, rank: int, world: int):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -385,7 +385,7 @@ def run_c4(args, rank: int, world: int):
     from paper_2411_17741_b200.model import CacheConfig, make_adapter_spec, zipf_catalog
     from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     ids, probs = zipf_catalog(1000)
     catalog = {a: make_adapter_spec(a, int(a[1:].split("-")[0])) for a in ids}
@@ -475,7 +475,7 @@ def run_c4(args, rank: int, world: int):
         torch.cuda.synchronize(dev)
     el = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([el], dtype=torch.float64, device=dev)
+        t = torch.tensor([el], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     hits, misses = cache.hits - h0, cache.misses - m0
@@ -531,8 +531,10 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        backend = "gloo" if args.impl == "reference" else "nccl"
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
+        # NCCL for the timing plumbing (the data path has no collective: replicas); gloo for the
+        # CPU reference arm, or by BENCH_DIST_BACKEND (e.g. several ranks sharing one GPU in a test)
+        backend = os.environ.get("BENCH_DIST_BACKEND") or ("gloo" if args.impl == "reference" else "nccl")
         dist.init_process_group(backend=backend)
     try:
         if args.impl == "reference":
