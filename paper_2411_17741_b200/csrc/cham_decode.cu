@@ -232,6 +232,10 @@ static_assert(TG == kSplitTG && NCB_SMALL == kSplitNcb, "split scratch geometry 
 #define CHAM_STAGGER 0  // 1: S(0) S(1) E(0) S(2) E(1) ... (A/B on C2: 103.5k vs 118.5k tok/s for S... E...)
 #endif
 constexpr bool kStagger = CHAM_STAGGER != 0;
+#ifndef CHAM_DEFER
+#define CHAM_DEFER 0  // 1: set aside one not-yet-ready expand unit instead of waiting on it
+#endif
+constexpr bool kDefer = CHAM_DEFER != 0;
 #ifndef CHAM_STAGGER_1JOB
 #define CHAM_STAGGER_1JOB 0  // stagger gap for single-projection launches only
 #endif
@@ -1321,16 +1325,45 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
   int4 da = make_int4(0, 0, 0, 0), db = da;
   int rdy = 0;
   if (unit >= 0) fetch(unit, up, da, db, rdy);
-  while (unit >= 0) {
+  // One expand unit whose tile was still in flight when its turn came may be set aside while
+  // the following units stream (its counter is re-read, relaxed, one unit ahead).
+  bool has_def = false;
+  int def_unit = 0, def_rdy = 0;
+  UnitPos def_up{};
+  int4 def_a = da, def_b = db;
+  auto peek = [&](const UnitPos& u) {
+    int v = 0;
+    if (lane == 0) {
+      const int* c = p.tile_ctr + u.job * NTL + u.di;
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    }
+    return v;
+  };
+  auto np_of = [](const int4& a) { return (a.z >> 8) & 0xff; };
+  while (unit >= 0 || has_def) {
+    if (has_def && (unit < 0 || __shfl_sync(0xffffffffu, def_rdy >= np_of(def_a), 0))) {
+      seq = issue_expand<T>(p, sm, seq, waited, fused, def_up.job, def_up.cc, def_up.di, def_up.half, def_up.tier, def_a,
+                            def_b, def_rdy, def_unit);
+      has_def = false;
+      if (unit < 0) break;
+    }
     const int nunit = uq.next(lane);
     UnitPos nup = up;
     int4 na = da, nb = db;
     int nrdy = 0;
     if (nunit >= 0) fetch(nunit, nup, na, nb, nrdy);
-    if (up.kind == KIND_SHRINK)
+    if (up.kind == KIND_SHRINK) {
       seq = issue_shrink<T>(p, sm, seq, waited, up.job, da, db);
-    else
+    } else if (kDefer && fused && !has_def && !__shfl_sync(0xffffffffu, rdy >= np_of(da), 0)) {
+      has_def = true;  // set aside; re-read below
+      def_unit = unit;
+      def_up = up;
+      def_a = da;
+      def_b = db;
+    } else {
       seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit);
+    }
+    if (has_def) def_rdy = peek(def_up);
     unit = nunit;
     up = nup;
     da = na;
