@@ -232,6 +232,9 @@ static_assert(TG == kSplitTG && NCB_SMALL == kSplitNcb, "split scratch geometry 
 #define CHAM_STAGGER 0  // 1: S(0) S(1) E(0) S(2) E(1) ... (A/B on C2: 103.5k vs 118.5k tok/s for S... E...)
 #endif
 constexpr bool kStagger = CHAM_STAGGER != 0;
+#ifndef CHAM_ASPLIT
+#define CHAM_ASPLIT 1  // bulk copies per shrink stage's A chunk
+#endif
 #ifndef CHAM_DEFER
 #define CHAM_DEFER 0  // 1: set aside one not-yet-ready expand unit instead of waiting on it
 #endif
@@ -1139,7 +1142,15 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
       m.kind = KIND_SHRINK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
       m.g = g; m.kc = kc;
       mbar_arrive_expect_tx(&sm.full[stage], a_bytes + x_bytes * tcount);
-      bulk_g2s(st, a_src + (long long)a0 * kAtomBytes, a_bytes, &sm.full[stage], pol_w);
+    }
+    __syncwarp();
+    {
+      // the A chunk as CHAM_ASPLIT copies issued by different lanes
+      const uint32_t part = a_bytes / CHAM_ASPLIT;
+      if (lane < CHAM_ASPLIT) {
+        const uint32_t nb = lane == CHAM_ASPLIT - 1 ? a_bytes - part * (CHAM_ASPLIT - 1) : part;
+        bulk_g2s(st + lane * part, a_src + (long long)a0 * kAtomBytes + lane * part, nb, &sm.full[stage], pol_w);
+      }
     }
     if (lane < tcount) m.rows[lane] = row;
     if (!waited) {  // x may be produced by the previous kernel
