@@ -1138,6 +1138,8 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
     const unsigned long long t_ready = p.trace ? gtimer() : 0;
     __syncwarp();
     Meta& m = sm.meta[stage];
+    if (lane < tcount) m.rows[lane] = row;
+    __syncwarp();  // every Meta store precedes lane 0's release-arrive below
     if (lane == 0) {
       m.kind = KIND_SHRINK; m.nst = nkc; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
       m.g = g; m.kc = kc;
@@ -1152,7 +1154,6 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
         bulk_g2s(st + lane * part, a_src + (long long)a0 * kAtomBytes + lane * part, nb, &sm.full[stage], pol_w);
       }
     }
-    if (lane < tcount) m.rows[lane] = row;
     if (!waited) {  // x may be produced by the previous kernel
       pdl_wait();
       pdl_launch_dependents();
@@ -1216,6 +1217,8 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       }
       __syncwarp();
       Meta& m = sm.meta[stage];
+      if (lane < tcount) m.rows[lane] = row;
+      __syncwarp();
       if (lane == 0) {
         m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
         m.pg0 = pe; m.npg = 0; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
@@ -1224,7 +1227,6 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
         bulk_g2s(st, p.split_buf + (long long)sidx * TG * ncol_unit, part_bytes * tcount, &sm.full[stage], pol_w);
       }
       if (lane < tcount) {
-        m.rows[lane] = row;
         bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
       }
       __syncwarp();
@@ -1255,13 +1257,14 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       __syncwarp();
     }
     Meta& m = sm.meta[stage];
+    if (lane < tcount) m.rows[lane] = row;
+    __syncwarp();  // every Meta store precedes lane 0's release-arrive below
     if (lane == 0) {
       m.kind = KIND_EXPAND; m.nst = nst; m.job = job; m.seg = s; m.pos0 = pos0; m.T = tcount; m.np = np;
       m.pg0 = pg0; m.npg = npg; m.col0 = col0; m.ncols = ncols; m.vrow = vrow;
       m.lpg = lpg; m.ncb = ncb; m.pitch = pitch; m.nq = ncb / 16; m.xm = xm; m.sidx = sidx;
       mbar_arrive_expect_tx(&sm.full[stage], bytes);
     }
-    if (lane < tcount) m.rows[lane] = row;
     // B pages of this stage (weights: independent of phase 1 and of the previous kernel)
     if (lane < npg) {
       const char* src = p.base + (long long)pgid * p.page_bytes + jb.b_off + (long long)col0 * ES * kRowsPerPage;

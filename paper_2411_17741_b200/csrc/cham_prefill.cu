@@ -36,9 +36,18 @@ namespace prefill {
 
 constexpr int BM = 128;                 // tokens per tile (UMMA M)
 constexpr int MAXR = kPrefillMaxRank;   // rank rows per adapter on this path
-constexpr int NS = 4;                   // ring stages
-constexpr int STAGE = 32768;            // bytes per ring stage
-constexpr int VBUF = 2 * BM * 128;      // V image: <= 2 K-blocks x 128 rows x 128 B
+#ifndef CHAM_PF_NS
+#define CHAM_PF_NS 4
+#endif
+#ifndef CHAM_PF_VBUF
+#define CHAM_PF_VBUF (2 * 128 * 128)
+#endif
+constexpr int NS = CHAM_PF_NS;          // ring stages
+#ifndef CHAM_PF_STAGE
+#define CHAM_PF_STAGE 32768
+#endif
+constexpr int STAGE = CHAM_PF_STAGE;    // bytes per ring stage
+constexpr int VBUF = CHAM_PF_VBUF;      // V images of one (job, tile): ks partials x K-blocks x mp rows x 128 B
 constexpr int CW = 512;                 // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
