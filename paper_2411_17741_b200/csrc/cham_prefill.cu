@@ -47,8 +47,15 @@ constexpr int NS = CHAM_PF_NS;          // ring stages
 #define CHAM_PF_STAGE 32768
 #endif
 constexpr int STAGE = CHAM_PF_STAGE;    // bytes per ring stage
+constexpr int VPAD = BM * 128 - 4096;   // worst over-read past a V buffer: 16 KiB - the smallest x block
 constexpr int VBUF = CHAM_PF_VBUF;      // V images of one (job, tile): ks partials x K-blocks x mp rows x 128 B
-constexpr int CW = 512;                 // expand unit columns
+#ifndef CHAM_PF_PDL
+#define CHAM_PF_PDL 1  // programmatic dependent launch for the prefill kernel
+#endif
+#ifndef CHAM_PF_CW
+#define CHAM_PF_CW 256  // expand unit width; A/B on C3: 256 -> 642k, 512 -> 625k, 1024 -> 553k tok/s
+#endif
+constexpr int CW = CHAM_PF_CW;          // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
 constexpr int MAX_TILES = kPrefillMaxTiles;
@@ -477,10 +484,10 @@ __device__ __forceinline__ int block_row(const Prefetch& f, const Unit& u, int b
 // ------------------------------------------------------------------ shared memory
 struct Shared {
   alignas(1024) unsigned char ring[NS][STAGE];
-  alignas(1024) unsigned char vbuf[2][VBUF];
-  // the UMMA A operand always spans 128 rows: the rows past a partial image's mp rows are
-  // read (and ignored) from whatever follows it, which must still be shared memory
-  unsigned char vpad[BM * 128 - 4096];
+  // The UMMA A operand always spans 128 rows: the rows past a partial image's mp rows are
+  // read (and ignored) from whatever follows it.  Each V buffer has its own pad so that read
+  // never overlaps the other buffer, which the loader may be filling (TMA) at the same time.
+  alignas(1024) unsigned char vbuf[2][VBUF + VPAD];
   uint64_t full[NS], empty[NS];
   uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[2], tempty_ex[2];
   uint64_t vfull[2], vempty[2];
@@ -985,6 +992,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             }
           }
         }
+        // the in-place y updates above are generic-proxy writes into a stage the loader will
+        // refill with TMA (async proxy): order them before the release
+        fence_proxy_async_shared();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[st]);
       }
@@ -1114,7 +1124,7 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = CHAM_PF_PDL ? 1 : 0;
   CHAM_CUDA(cudaLaunchKernelEx(&cfg, fused_kernel, prm));
   return CHAM_OK;
 }
