@@ -1113,9 +1113,53 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
   return r;
 }
 
+#ifndef CHAM_EARLY_A
+#define CHAM_EARLY_A 0  // 1: A chunks of the whole first ring pass before griddepcontrol.wait (C2 114.0k vs 115.2k off)
+#endif
+// x copies of the first ring pass held back until the previous kernel has completed, so the
+// adapter (A) parts of up to NSTAGE stages stream while that kernel drains.  Per lane: its x
+// row's source; the stage, barrier and size are uniform.
+struct PendingX {
+  const char* src[NSTAGE];
+  uint32_t dst[NSTAGE];
+  uint32_t bar[NSTAGE];
+  uint32_t bytes[NSTAGE];
+  bool on[NSTAGE];
+  int n;
+};
+__device__ __forceinline__ void pend_add(PendingX& q, const char* src, void* dst, uint64_t* bar, uint32_t bytes, bool on) {
+#pragma unroll
+  for (int i = 0; i < NSTAGE; ++i)
+    if (i == q.n) {
+      q.src[i] = src;
+      q.dst[i] = smem_u32(dst);
+      q.bar[i] = smem_u32(bar);
+      q.bytes[i] = bytes;
+      q.on[i] = on;
+    }
+  ++q.n;
+}
+// wait for the previous kernel (x, y and the workspaces may be its outputs), then issue the
+// held-back x copies
+__device__ __forceinline__ void pend_flush(PendingX& q, bool& waited, uint64_t pol_x) {
+  if (waited) return;
+  pdl_wait();
+  pdl_launch_dependents();
+  waited = true;
+#pragma unroll
+  for (int i = 0; i < NSTAGE; ++i)
+    if (i < q.n && q.on[i])
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+          "[%0], [%1], %2, [%3], %4;" ::"r"(q.dst[i]),
+          "l"(q.src[i]), "r"(q.bytes[i]), "r"(q.bar[i]), "l"(pol_x)
+          : "memory");
+  q.n = 0;
+}
+
 template <typename T>
-__device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq, bool& waited, int job, int4 da,
-                                            int4 db) {
+__device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq, bool& waited, PendingX& pend, int job,
+                                            int4 da, int4 db) {
   constexpr int ES = Elem<T>::kBytes;
   const int lane = threadIdx.x & 31;
   const int nkc = n_kchunks<T>(p);
@@ -1134,6 +1178,8 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
     const uint32_t a_bytes = min(A_CHUNK / kAtomBytes, natoms - a0) * kAtomBytes;
     const uint32_t x_bytes = a_bytes / kRowsPerPage;
     unsigned char* st = sm.stage[stage];
+    // a stage's second use waits for consumers that need their x rows: release them first
+    if (seq >= NSTAGE) pend_flush(pend, waited, pol_x);
     if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
     const unsigned long long t_ready = p.trace ? gtimer() : 0;
     __syncwarp();
@@ -1154,14 +1200,13 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
         bulk_g2s(st + lane * part, a_src + (long long)a0 * kAtomBytes + lane * part, nb, &sm.full[stage], pol_w);
       }
     }
-    if (!waited) {  // x may be produced by the previous kernel
-      pdl_wait();
-      pdl_launch_dependents();
-      waited = true;
+    const char* x_src = jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW;
+    if (!waited && CHAM_EARLY_A) {  // x may be produced by the previous kernel: hold it back
+      pend_add(pend, x_src, st + A_CHUNK + lane * X_PITCH, &sm.full[stage], x_bytes, lane < tcount);
+    } else {
+      pend_flush(pend, waited, pol_x);
+      if (lane < tcount) bulk_g2s(st + A_CHUNK + lane * X_PITCH, x_src, x_bytes, &sm.full[stage], pol_x);
     }
-    if (lane < tcount)
-      bulk_g2s(st + A_CHUNK + lane * X_PITCH, jb.x + ((long long)row * p.h_in) * ES + (long long)kc * X_ROW, x_bytes,
-               &sm.full[stage], pol_x);
     if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
     __syncwarp();
   }
@@ -1169,10 +1214,11 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
 }
 
 template <typename T>
-__device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq, bool& waited, bool fused, int job,
-                                            int cc, int tile, int half, int tier, int4 da, int4 db, int rdy,
-                                            int unit) {
+__device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq, bool& waited, PendingX& pend,
+                                            bool fused, int job, int cc, int tile, int half, int tier, int4 da,
+                                            int4 db, int rdy, int unit) {
   constexpr int ES = Elem<T>::kBytes;
+  pend_flush(pend, waited, policy_evict_last());
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
   const int NTL = pl.totals[1];
@@ -1313,6 +1359,8 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
 
 template <typename T>
 __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq, bool& waited, int mode) {
+  PendingX pend;
+  pend.n = 0;
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
   const bool fused = mode == MODE_FUSED;
@@ -1356,7 +1404,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
   auto np_of = [](const int4& a) { return (a.z >> 8) & 0xff; };
   while (unit >= 0 || has_def) {
     if (has_def && (unit < 0 || __shfl_sync(0xffffffffu, def_rdy >= np_of(def_a), 0))) {
-      seq = issue_expand<T>(p, sm, seq, waited, fused, def_up.job, def_up.cc, def_up.di, def_up.half, def_up.tier, def_a,
+      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, def_up.job, def_up.cc, def_up.di, def_up.half, def_up.tier, def_a,
                             def_b, def_rdy, def_unit);
       has_def = false;
       if (unit < 0) break;
@@ -1367,7 +1415,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
     int nrdy = 0;
     if (nunit >= 0) fetch(nunit, nup, na, nb, nrdy);
     if (up.kind == KIND_SHRINK) {
-      seq = issue_shrink<T>(p, sm, seq, waited, up.job, da, db);
+      seq = issue_shrink<T>(p, sm, seq, waited, pend, up.job, da, db);
     } else if (kDefer && fused && !has_def && !__shfl_sync(0xffffffffu, rdy >= np_of(da), 0)) {
       has_def = true;  // set aside; re-read below
       def_unit = unit;
@@ -1375,7 +1423,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
       def_a = da;
       def_b = db;
     } else {
-      seq = issue_expand<T>(p, sm, seq, waited, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit);
+      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit);
     }
     if (has_def) def_rdy = peek(def_up);
     unit = nunit;
@@ -1384,6 +1432,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
     db = nb;
     rdy = nrdy;
   }
+  pend_flush(pend, waited, policy_evict_last());
   return seq;
 }
 
