@@ -513,6 +513,140 @@ def run_c4(args, rank: int, world: int):
     pool.close()
 
 
+# --------------------------------------------------------------------------- C5: tensor parallel
+H70, L70 = 8192, 80
+H70_IN = [8192, 8192, 8192, 8192]   # q, k, v, o
+H70_OUT = [8192, 1024, 1024, 8192]  # GQA: 8 KV heads
+C5_ADAPTERS, C5_RANK = 100, 64
+
+
+def run_c5(args, rank: int, world: int):
+    """C5: Llama-2-70B dims (80 layers; q/o 8192->8192, k/v 8192->1024), 100 adapters of rank 64,
+    decode batch of 256 tokens, tensor parallel over the N ranks (TP = N; every rank sees the
+    same tokens).  A step = per layer: shrink of the rank's x shard for q/k/v into one fused
+    [T, 3 x 64] fp32 v, ONE all-reduce of it, expand into the rank's y shards; then the same for
+    o (its own all-reduce): 160 all-reduces per step at N > 1 (tp.py).  The step is
+    one CUDA graph (NCCL all-reduces captured); value = tokens/s of the TP group."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_17741_b200.executor import segment_token_bounds
+    from paper_2411_17741_b200.ops import build_plan, build_segments
+    from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
+    from paper_2411_17741_b200.tp import TensorParallelLora, shard_dims
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
+    torch.cuda.set_device(dev)
+    hin_l, hout_l = shard_dims(H70_IN, H70_OUT, world)
+    npg = pages_for_rank(C5_RANK)
+    pool = AdapterPool(C5_ADAPTERS * npg, L70, hin_l, hout_l, dtype=torch.bfloat16, n_slots=C5_ADAPTERS,
+                       max_tokens=T_DECODE, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321 + rank)
+    for a in range(C5_ADAPTERS):
+        pool.set_slot(a, C5_RANK, list(range(a * npg, (a + 1) * npg)))
+        buf = (torch.randn(npg * pool.page_bytes // 2, generator=gen, device=dev) * 0.02).to(torch.bfloat16)
+        pool.fill_from_device(a, buf.view(torch.uint8))
+        del buf
+    torch.cuda.synchronize(dev)
+    # the same decode batch on every TP rank: 256 requests, adapters uniform over the catalog
+    req_slot = np.random.default_rng(0).integers(0, C5_ADAPTERS, T_DECODE).astype(np.int32)
+    req_rank = np.full(T_DECODE, C5_RANK, dtype=np.int32)
+    # host routing hints (as LoraStepExecutor.upload passes them): every segment is decode-sized,
+    # so no launch of the step needs the prefill kernel family
+    lo, hi = segment_token_bounds(req_slot, req_rank, np.ones(T_DECODE, dtype=np.int32))
+    pool.set_prefill_route(64, lo, hi)
+    table = build_segments(req_slot, req_rank, np.ones(T_DECODE, dtype=np.int32), device=dev)
+    n_seg = int(table.n_seg.item())
+    table.n_seg_host = n_seg
+    build_plan(table, pool=pool)
+    groups = [[0, 1, 2], [3]]
+    group = dist.group.WORLD if world > 1 else False
+    tp = TensorParallelLora(pool, max_tokens=T_DECODE, r_stride=C5_RANK, proj_groups=groups, group=group, device=dev)
+    xs = [[torch.randn(T_DECODE, hin_l[g[0]], device=dev).to(torch.bfloat16) for g in groups] for _ in range(L70)]
+    ys = [[torch.randn(T_DECODE, hout_l[p], device=dev).to(torch.bfloat16) for p in range(4)] for _ in range(L70)]
+    kw = dict(perm=table.perm[:T_DECODE], n_positions=T_DECODE, plan=table.plan)
+
+    def step(stream):
+        for layer in range(L70):
+            for gi, projs in enumerate(groups):
+                tp.apply_group(layer, projs, xs[layer][gi], [ys[layer][p] for p in projs],
+                               table.seg_slot[:n_seg], table.seg_off[:n_seg + 1], table.seg_rank[:n_seg],
+                               stream=stream, **kw)
+
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        step(s)  # eager warm-up (kernel attributes, NCCL communicator)
+    torch.cuda.synchronize(dev)
+    graph = None
+    if world == 1 or dist.get_backend() == "nccl":
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            step(s)
+        torch.cuda.synchronize(dev)
+
+    def run_steps(n):
+        with torch.cuda.stream(s):
+            for _ in range(n):
+                if graph is not None:
+                    graph.replay()
+                else:
+                    step(s)
+
+    run_steps(args.warmup)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        ev0.record(s)
+        run_steps(args.steps)
+        ev1.record(s)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    # algorithmic bytes of this rank's shard (SURVEY §8d per (layer, proj), local dims)
+    perm, off, sl, rk = table.to_host()
+    bytes_rank = 0
+    adapter_rank = 0
+    for p in range(4):
+        a_b, act_b = algorithmic_bytes(off, sl, rk, T_DECODE, hin_l[p], hout_l[p], 2)
+        bytes_rank += (int(a_b) + int(act_b)) * L70
+        adapter_rank += int(a_b) * L70
+    hbm_peak, _, peak_kind = peaks()
+    achieved = bytes_rank / (step_ms * 1e-3) / 1e9
+    if rank == 0:
+        distinct = len(set(req_slot.tolist()))
+        line = {
+            "metric": METRIC, "value": T_DECODE / (step_ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"C5: Llama-2-70B dims LoRA (80 layers, q/o 8192->8192, k/v 8192->1024), "
+                                   f"{C5_ADAPTERS} adapters of rank {C5_RANK} ({distinct} distinct in the batch), "
+                                   f"decode batch {T_DECODE} tokens, TP={world}",
+                       "global_batch": T_DECODE, "seq_len": 1, "parallelism": f"tp{world}",
+                       "collectives_per_step": 2 * L70 if world > 1 else 0,
+                       "l2": "inputs larger than L2: each step streams the shards of every distinct adapter"},
+            "adapter_read_gbs_per_rank": adapter_rank / (step_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                         "kernel": "decode::lora_apply_kernel<bf16> MODE_SHRINK / MODE_EXPAND around the all-reduce "
+                                   "(rank 0's step incl. collectives)",
+                         "bytes_per_step_per_rank": bytes_rank, "launches_per_step": L70 * 8},
+            "gpu_launches": args.steps * L70 * 8,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    pool.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -520,7 +654,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["qkv", "per-proj"], default="qkv")
-    ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c2",
+    ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c2",
                     help="c2 (default, the BASELINE metric's decode config) or c3 (prefill, tcgen05 path)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -541,6 +675,8 @@ def main():
             run_reference(args, rank, world)
         elif args.config == "c4":
             run_c4(args, rank, world)
+        elif args.config == "c5":
+            run_c5(args, rank, world)
         else:
             run_ours(args, rank, world)
     finally:

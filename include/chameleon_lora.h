@@ -191,6 +191,20 @@ CHAM_API int cham_lora_expand(cham_pool* pool, int layer, int proj, const float*
                      void* y, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
                      const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream);
 
+/* Tensor-parallel halves over several projections of one layer in ONE launch each: job j
+ * (projection projs[j]) owns v columns [j * v_cols, (j + 1) * v_cols) of every v row, so the
+ * q/k/v shrink outputs land side by side in the single buffer that is all-reduced.  shrink:
+ * the projections must share h_in; expand: they must share h_out.  n_jobs <= 4,
+ * n_jobs * v_cols <= v_stride, v_cols a multiple of 4; ranks beyond v_cols are dropped. */
+CHAM_API int cham_lora_shrink_multi(cham_pool* pool, int layer, int n_jobs, const int* projs,
+                     const void* const* xs, float* v, int v_stride, int v_cols, int n_tokens,
+                     const int* perm, const int* seg_off, const int* seg_slot, const int* seg_rank,
+                     int n_seg, const int* n_seg_dev, const void* plan, void* stream);
+CHAM_API int cham_lora_expand_multi(cham_pool* pool, int layer, int n_jobs, const int* projs,
+                     const float* v, int v_stride, int v_cols, void* const* ys, int n_tokens,
+                     const int* perm, const int* seg_off, const int* seg_slot, const int* seg_rank,
+                     int n_seg, const int* n_seg_dev, const void* plan, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,10 @@ SIGNATURES = {
                                       c_int, _P, _P, _P]),
     "cham_lora_shrink": (c_int, [_P, c_int, c_int, _P, _P, c_int, c_int, _P, _P, _P, _P, c_int, _P, _P, _P]),
     "cham_lora_expand": (c_int, [_P, c_int, c_int, _P, c_int, _P, c_int, _P, _P, _P, _P, c_int, _P, _P, _P]),
+    "cham_lora_shrink_multi": (c_int, [_P, c_int, c_int, _P, _P, _P, c_int, c_int, c_int, _P, _P, _P, _P, c_int, _P,
+                                       _P, _P]),
+    "cham_lora_expand_multi": (c_int, [_P, c_int, c_int, _P, _P, c_int, c_int, _P, c_int, _P, _P, _P, _P, c_int, _P,
+                                       _P, _P]),
 }
 
 _lib = None

@@ -28,9 +28,13 @@
 //    grid is one CTA per SM (co-resident).  Every CTA executes griddepcontrol.wait before
 //    exiting, so apply n completes after apply n-1 and the ping-pong v buffer of apply
 //    n-2 is free when apply n writes it.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "cham_pool.h"
 
 namespace cham {
+int encode_f32_map(CUtensorMap* m, const void* base, int rows, int cols, int pitch, int box_cols, int box_rows);
 int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
                    void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
                    const int* seg_rank, int n_seg, const int* n_seg_dev, void* stream, int mode, float* v_out,
@@ -121,6 +125,7 @@ struct Job {
 };
 
 struct Params {
+  CUtensorMap vmap;   // MODE_EXPAND: v_in as [positions][v_stride] fp32, boxes of 8 ranks x TG tokens
   const char* base;
   long long page_bytes;
   const int* slot_pages;
@@ -145,6 +150,7 @@ struct Params {
   float* v_out;       // MODE_SHRINK: v [positions][v_stride]
   const float* v_in;  // MODE_EXPAND: v [positions][v_stride]
   int v_stride;
+  int v_cols;         // columns of one job's v slice: job j's v starts at column j * v_cols
   unsigned long long* trace;  // debug: [cta][seq][8] globaltimer stamps (null = off)
   int trace_cap;
   const void* plan;           // Plan header + unit descriptors (cham_build_plan)
@@ -249,7 +255,8 @@ struct Schedule {
   int a[MAX_BLOCKS], e[MAX_BLOCKS];  // LPT positions [a, e) of the class
 };
 
-constexpr int STAGE_BYTES = K1_STAGE > K2_STAGE ? K1_STAGE : K2_STAGE;
+// rounded to 128 B: every stage base must satisfy the TMA tensor-copy alignment (TP v boxes)
+constexpr int STAGE_BYTES = ((K1_STAGE > K2_STAGE ? K1_STAGE : K2_STAGE) + 127) / 128 * 128;
 constexpr int SCRATCH_BYTES = TG * kMaxRank * 4;  // K2 v rows; K1 uses the first 1 KiB
 struct Shared {
   alignas(128) unsigned char stage[NSTAGE][STAGE_BYTES];
@@ -661,7 +668,7 @@ __device__ __forceinline__ void shrink_unit_mma(const Params& p, const Plan& pl,
     for (int w2 = 0; w2 < GROUP_WARPS; ++w2) sum += red[(w2 * TG + t) * kRowsPerPage + j];
     const int row = m0.g * kRowsPerPage + j;
     if (p.v_out) {
-      if (row < p.v_stride) p.v_out[(long long)(m0.pos0 + t) * p.v_stride + row] = sum;  // TP [position][v_stride]
+      if (row < p.v_cols) p.v_out[(long long)(m0.pos0 + t) * p.v_stride + m0.job * p.v_cols + row] = sum;  // TP
     } else {
       const int tile = (m0.pos0 - pl.seg_off[m0.seg]) / TG;
       const long long vb = pl.v_start[m0.seg] + (long long)tile * TG * m0.np * kRowsPerPage;
@@ -736,7 +743,7 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
     if (t < NT) {
       const int row = m0.g * kRowsPerPage + j;
       if (p.v_out) {
-        if (row < p.v_stride) p.v_out[(long long)(m0.pos0 + t) * p.v_stride + row] = sum;  // TP [position][v_stride]
+        if (row < p.v_cols) p.v_out[(long long)(m0.pos0 + t) * p.v_stride + m0.job * p.v_cols + row] = sum;  // TP
       } else {
         // tile-major layout [page][TG][8 rows]: each expand stage copies its pages' slice
         const int tile = (m0.pos0 - pl.seg_off[m0.seg]) / TG;
@@ -1241,7 +1248,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
   const uint32_t b_bytes = ncols * ES * kRowsPerPage;  // per page
   const uint32_t y_bytes = ncols * ES;                  // per token
   const int rpad = np * kRowsPerPage;
-  const int vrow = p.v_in ? min(rpad, p.v_stride) : rpad;
+  const int vrow = p.v_in ? min(rpad, p.v_cols) : rpad;
   // page range of this unit: all pages, or one half of them (the second half adds a combine stage)
   const int pb = half == 1 ? np / 2 : 0, pe = half == 0 ? np / 2 : np;
   const int nst_pg = ceil_div(pe - pb, pgs);
@@ -1284,7 +1291,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
     // every stage carries its pages' v slice; the last one also the y rows.  With a
     // caller-provided v (TP) only pages inside v_stride are copied, the rest are zeroed.
     const int npg_in = p.v_in ? max(0, min(npg, vrow / kRowsPerPage - pg0)) : npg;
-    const uint32_t v_bytes = p.v_in ? npg_in * tcount * kRowsPerPage * 4 : npg * TG * kRowsPerPage * 4;
+    const uint32_t v_bytes = p.v_in ? npg_in * TG * kRowsPerPage * 4 : npg * TG * kRowsPerPage * 4;
     uint32_t bytes = b_bytes * npg + v_bytes;
     if (y_here) bytes += y_bytes * tcount;
     int pgid = 0;
@@ -1334,13 +1341,15 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       __syncwarp();
     }
     if (p.v_in) {
-      // TP: v [position][v_stride] -> stage [page][token][8], one 32-byte copy each
-      for (int c2 = lane; c2 < npg_in * tcount; c2 += 32) {
-        const int hh = c2 / tcount, t = c2 - hh * tcount;
-        const int r0 = (pg0 + hh) * kRowsPerPage;
-        bulk_g2s(st + K2_V + (hh * TG + t) * kRowsPerPage * 4, p.v_in + (long long)(pos0 + t) * p.v_stride + r0,
-                 kRowsPerPage * 4, &sm.full[stage], pol_w);
-      }
+      // TP: v [position][v_stride] -> stage [page][token][8]: one 2-D box (8 ranks x TG
+      // positions; rows past the tile are read and ignored, past the buffer zero-filled) per page
+      if (lane < npg_in)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(st + K2_V + lane * TG * kRowsPerPage * 4)),
+            "l"(reinterpret_cast<uint64_t>(&p.vmap)), "r"(job * p.v_cols + (pg0 + lane) * kRowsPerPage), "r"(pos0),
+            "r"(smem_u32(&sm.full[stage])), "l"(pol_w)
+            : "memory");
     } else if (lane == 0) {
       bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase + pg0 * TG * kRowsPerPage, v_bytes, &sm.full[stage],
                pol_w);
@@ -1653,7 +1662,7 @@ int build_plan_entry(cham_pool* pool, const int* perm, const int* seg_off, const
 int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,
                  void* const* ys, int n_tokens, const int* perm, const int* seg_off, const int* seg_slot,
                  const int* seg_rank, int n_seg, const int* n_seg_dev, const void* plan, void* stream, int mode,
-                 float* v_out, const float* v_in, int v_stride) {
+                 float* v_out, const float* v_in, int v_stride, int v_cols) {
   using namespace decode;
   if (!pool) return fail(CHAM_ERR_INVALID, "lora_apply: null pool");
   if (layer < 0 || layer >= pool->n_layers) return fail(CHAM_ERR_INVALID, "lora_apply: layer out of range");
@@ -1664,9 +1673,11 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   if (n_seg > PLAN_SEGS) return fail(CHAM_ERR_LIMIT, "lora_apply: too many segments");
   if (n_tokens < 0 || n_tokens > pool->max_tokens)
     return fail(CHAM_ERR_LIMIT, "lora_apply: n_tokens exceeds the pool's max_tokens");
-  if (mode != MODE_FUSED && n_jobs != 1) return fail(CHAM_ERR_INVALID, "shrink/expand take one projection");
   if ((v_in || v_out) && (v_stride <= 0 || v_stride % 4))
     return fail(CHAM_ERR_INVALID, "lora_shrink/expand: v_stride must be a positive multiple of 4");
+  if (v_cols <= 0) v_cols = v_stride;
+  if ((v_in || v_out) && (v_cols % 4 || (long long)n_jobs * v_cols > v_stride))
+    return fail(CHAM_ERR_INVALID, "lora_shrink/expand: v_cols must be a multiple of 4 with n_jobs * v_cols <= v_stride");
   Params prm{};
   prm.base = pool->base;
   prm.page_bytes = (long long)pool->page_bytes;
@@ -1679,8 +1690,9 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   for (int j = 0; j < n_jobs; ++j) {
     const int pj = projs[j];
     if (pj < 0 || pj >= pool->n_proj) return fail(CHAM_ERR_INVALID, "lora_apply: proj out of range");
-    if (pool->h_in[pj] != prm.h_in || pool->h_out[pj] != prm.h_out)
-      return fail(CHAM_ERR_INVALID, "lora_apply_multi: projections must share h_in and h_out");
+    // shrink reads only h_in, expand only h_out; the fused apply needs both equal
+    if ((mode != MODE_EXPAND && pool->h_in[pj] != prm.h_in) || (mode != MODE_SHRINK && pool->h_out[pj] != prm.h_out))
+      return fail(CHAM_ERR_INVALID, "lora_apply_multi: projections must share h_in (shrink) / h_out (expand)");
     const int lp = layer * pool->n_proj + pj;
     if (mode != MODE_EXPAND && !xs[j]) return fail(CHAM_ERR_INVALID, "lora_apply: null x");
     if (mode != MODE_SHRINK && !ys[j]) return fail(CHAM_ERR_INVALID, "lora_apply: null y");
@@ -1701,6 +1713,11 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   prm.v_out = mode == MODE_SHRINK ? v_out : nullptr;
   prm.v_in = mode == MODE_EXPAND ? v_in : nullptr;
   prm.v_stride = v_stride;
+  prm.v_cols = v_cols;
+  if (prm.v_in) {
+    const int rc = encode_f32_map(&prm.vmap, v_in, n_tokens, v_stride, v_stride, kRowsPerPage, TG);
+    if (rc) return rc;
+  }
   prm.trace = pool->d_trace;
   prm.trace_cap = pool->trace_cap;
   prm.desc_cap = plan_desc_capacity(pool->max_tokens);
@@ -1713,6 +1730,16 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   prm.plan = plan;
   prm.prefill_thr = prefill_route_thr(pool);
   const bool pre = prm.prefill_thr < (1 << 30) && n_tokens >= prm.prefill_thr;
+  if (pre && mode != MODE_FUSED && n_jobs > 1) {
+    // the prefill kernel's TP halves take one projection: one call per job on its v columns
+    for (int j = 0; j < n_jobs; ++j) {
+      const int rc = decode_entry(pool, layer, 1, projs + j, xs + j, ys + j, n_tokens, perm, seg_off, seg_slot,
+                                  seg_rank, n_seg, n_seg_dev, plan, stream, mode, v_out ? v_out + j * v_cols : nullptr,
+                                  v_in ? v_in + j * v_cols : nullptr, v_stride, v_cols);
+      if (rc) return rc;
+    }
+    return CHAM_OK;
+  }
   // with a host guarantee that every segment is prefill-sized, the decode kernel has no work
   const bool dec = !pre || pool->route_min_seg < prm.prefill_thr;
   int rc = CHAM_OK;

@@ -1052,6 +1052,22 @@ int encode_act_map(CUtensorMap* m, const void* base, int rows, int cols, int box
 }
 }  // namespace
 
+// [rows x cols] fp32 row-major (row pitch `pitch` floats), unswizzled boxes of box_cols x
+// box_rows: the decode kernel's TP v operand (one box = one page's 8 ranks of a token tile).
+int encode_f32_map(CUtensorMap* m, const void* base, int rows, int cols, int pitch, int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CHAM_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHAM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CHAM_OK;
+}
+
 // Launch the fused tcgen05 kernel for the prefill segments of this apply.
 // mode: 0 fused, 1 shrink only (v_out, TP), 2 expand only (v_in, TP).
 int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, const void* const* xs,

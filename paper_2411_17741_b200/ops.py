@@ -199,3 +199,47 @@ def lora_expand(v: torch.Tensor, y: torch.Tensor, slot_ids, seg_offsets, ranks, 
          int(y.shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
          ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))
     return y
+
+
+def _multi_v_check(v: torch.Tensor, n: int) -> int:
+    """v: the fused fp32 [positions, n * v_cols] buffer (column slice views accepted)."""
+    _check_v(v)
+    if v.shape[1] % n or (v.shape[1] // n) % 4:
+        raise ValueError("v columns must split into len(projs) slices of a multiple of 4 columns")
+    return v.shape[1] // n
+
+
+def lora_shrink_multi(xs: Sequence[torch.Tensor], v: torch.Tensor, slot_ids, seg_offsets, ranks, *,
+                      pool: AdapterPool, layer: int, projs: Sequence[int], perm=None, n_seg: Optional[int] = None,
+                      plan=None, stream=None) -> torch.Tensor:
+    """v[k, j*c:(j+1)*c][:r] = x_j[perm[k]] . A_slot(projs[j]) for every j in ONE launch, c =
+    v.shape[1] / len(projs) (the TP all-reduce operand of a projection group sharing h_in)."""
+    n = len(projs)
+    if len(xs) != n:
+        raise ValueError("xs and projs must have equal length")
+    for x, p in zip(xs, projs):
+        _check_act(x, pool, pool.h_in[p], "x")
+    cols = _multi_v_check(v, n)
+    ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
+    xa = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
+    call("cham_lora_shrink_multi", pool.handle, int(layer), n, _lib.int_array(projs), xa, v.data_ptr(),
+         int(v.stride(0)), cols, int(xs[0].shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
+         ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))
+    return v
+
+
+def lora_expand_multi(v: torch.Tensor, ys: Sequence[torch.Tensor], slot_ids, seg_offsets, ranks, *,
+                      pool: AdapterPool, layer: int, projs: Sequence[int], perm=None, n_seg: Optional[int] = None,
+                      plan=None, stream=None):
+    """y_j[perm[k]] += v[k, j*c:(j+1)*c] . B_slot(projs[j]) for every j in ONE launch (shared h_out)."""
+    n = len(projs)
+    if len(ys) != n:
+        raise ValueError("ys and projs must have equal length")
+    for y, p in zip(ys, projs):
+        _check_act(y, pool, pool.h_out[p], "y")
+    cols = _multi_v_check(v, n)
+    ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
+    ya = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
+    call("cham_lora_expand_multi", pool.handle, int(layer), n, _lib.int_array(projs), v.data_ptr(), int(v.stride(0)),
+         cols, ya, int(ys[0].shape[0]), _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(),
+         ss.numel() if n_seg is None else int(n_seg), None, _lib.ptr(plan), _stream_ptr(stream))

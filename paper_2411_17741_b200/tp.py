@@ -72,6 +72,9 @@ class TensorParallelLora:
         self.group = group
         self.shrink = shrink or ops.lora_shrink
         self.expand = expand or ops.lora_expand
+        # the device operators also come as multi-projection launches (one shrink for the
+        # whole group, one expand per run of projections sharing h_out)
+        self.multi = shrink is None and expand is None
         width = max(len(g) for g in self.proj_groups) * self.r_stride
         dev = device if device is not None else pool.device
         # flat storage: each group's operand is a CONTIGUOUS [n_pos, len(group) * r_stride] view
@@ -93,9 +96,12 @@ class TensorParallelLora:
         n_pos = T if n_positions is None else int(n_positions)
         R = self.r_stride
         v = self.v[: n_pos * len(projs) * R].view(n_pos, len(projs) * R)
-        for i, p in enumerate(projs):
-            self.shrink(x, v[:, i * R:(i + 1) * R], slot_ids, seg_offsets, ranks, pool=self.pool, layer=layer,
-                        proj=p, perm=perm, plan=plan, stream=stream)
+        tables = dict(pool=self.pool, layer=layer, perm=perm, plan=plan, stream=stream)
+        if self.multi and len(projs) > 1 and len({self.pool.h_in[p] for p in projs}) == 1:
+            ops.lora_shrink_multi([x] * len(projs), v, slot_ids, seg_offsets, ranks, projs=list(projs), **tables)
+        else:
+            for i, p in enumerate(projs):
+                self.shrink(x, v[:, i * R:(i + 1) * R], slot_ids, seg_offsets, ranks, proj=p, **tables)
         if self.group is not False and dist.is_initialized() and dist.get_world_size(self.group) > 1:
             if stream is not None:
                 with torch.cuda.stream(stream):
@@ -103,9 +109,18 @@ class TensorParallelLora:
             else:
                 dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
             self.allreduce_count += 1
-        for i, p in enumerate(projs):
-            self.expand(v[:, i * R:(i + 1) * R], ys[i], slot_ids, seg_offsets, ranks, pool=self.pool, layer=layer,
-                        proj=p, perm=perm, plan=plan, stream=stream)
+        i = 0
+        while i < len(projs):
+            j = i + 1
+            if self.multi:  # the run of projections from i sharing h_out
+                while j < len(projs) and self.pool.h_out[projs[j]] == self.pool.h_out[projs[i]]:
+                    j += 1
+            if j - i > 1:
+                ops.lora_expand_multi(v[:, i * R:j * R], list(ys[i:j]), slot_ids, seg_offsets, ranks,
+                                      projs=list(projs[i:j]), **tables)
+            else:
+                self.expand(v[:, i * R:(i + 1) * R], ys[i], slot_ids, seg_offsets, ranks, proj=projs[i], **tables)
+            i = j
 
     def apply_layer(self, layer: int, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], slot_ids,
                     seg_offsets, ranks, **kw) -> None:

@@ -375,3 +375,63 @@ def test_page_half_split_expand_units(dtype):
         np.testing.assert_allclose(got, ref, rtol=FP32_RTOL, atol=1e-5)
     else:
         np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+@pytest.mark.parametrize("ntok", ["decode", "mixed"])
+def test_tp2_multi_projection_halves(ntok):
+    """The TP halves as multi-projection launches (cham_lora_shrink_multi / _expand_multi):
+    q/k/v (k/v GQA-narrow) shrink into ONE fused [n_pos, 3R] v per rank, the emulated
+    all-reduce sums the two ranks' buffers, expand runs q alone and k+v in one launch.  The
+    concatenated y shards must equal the unsharded oracle.  "mixed" adds a 96-token segment,
+    which routes through the prefill kernel (one launch per projection there)."""
+    from paper_2411_17741_b200.ops import lora_expand, lora_expand_multi, lora_shrink_multi
+    from paper_2411_17741_b200.tp import shard_bounds
+
+    rng = np.random.default_rng(12)
+    H_IN, H_OUT = [2048, 2048, 2048], [2048, 256, 256]
+    slot_ranks = {0: 64, 1: 40, 2: 16, 3: 64}
+    full = [make_adapters(rng, slot_ranks, H_IN[p], H_OUT[p], bf16=True) for p in range(3)]
+    n_req = 40
+    req_slots = rng.integers(0, 4, n_req).tolist()
+    req_ntok = [1] * n_req if ntok == "decode" else [1] * (n_req - 1) + [96]
+    req_rank = [slot_ranks[s] for s in req_slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(req_slots, req_rank, req_ntok)
+    T = int(sum(req_ntok))
+    x = bf16_round(rng.standard_normal((T, 2048)).astype(np.float32))
+    ys = [bf16_round(rng.standard_normal((T, H_OUT[p])).astype(np.float32)) for p in range(3)]
+    R, world = 64, 2
+    n_pos = int(seg_off[-1])
+    vs, pools, yd = [], [], []
+    for rank in range(world):
+        i0, i1 = shard_bounds(2048, world, rank)
+        pool = _pool(1, [1024] * 3, [h // world for h in H_OUT], torch.bfloat16, 4 * 8, max_tokens=256)
+        sh = {}
+        for s in slot_ranks:
+            sh[s] = []
+            for p in range(3):
+                o0, o1 = shard_bounds(H_OUT[p], world, rank)
+                a, b = full[p][s]
+                sh[s].append((np.ascontiguousarray(a[i0:i1]), np.ascontiguousarray(b[:, o0:o1])))
+        _install(pool, sh, slot_ranks)
+        xd = torch.from_numpy(x[:, i0:i1].copy()).to("cuda", torch.bfloat16)
+        v = torch.full((n_pos, 3 * R), float("nan"), dtype=torch.float32, device="cuda")
+        v.zero_()
+        lora_shrink_multi([xd] * 3, v, seg_slot, seg_off, seg_rank, pool=pool, layer=0, projs=[0, 1, 2], perm=perm)
+        vs.append(v)
+        pools.append(pool)
+        yd.append([torch.from_numpy(ys[p][:, shard_bounds(H_OUT[p], world, rank)[0]:
+                                            shard_bounds(H_OUT[p], world, rank)[1]].copy()).to("cuda", torch.bfloat16)
+                   for p in range(3)])
+    v_sum = vs[0] + vs[1]  # the all-reduce
+    for rank in range(world):
+        lora_expand(v_sum[:, :R], yd[rank][0], seg_slot, seg_off, seg_rank, pool=pools[rank], layer=0, proj=0,
+                    perm=perm)
+        lora_expand_multi(v_sum[:, R:], yd[rank][1:], seg_slot, seg_off, seg_rank, pool=pools[rank], layer=0,
+                          projs=[1, 2], perm=perm)
+    torch.cuda.synchronize()
+    for p in range(3):
+        got = torch.cat([yd[r][p] for r in range(world)], dim=1).float().cpu().numpy()
+        ref = lora_apply_ref(x, ys[p], perm, seg_off, seg_slot, seg_rank, full[p])
+        np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+    for pool in pools:
+        pool.close()
