@@ -435,3 +435,58 @@ def test_tp2_multi_projection_halves(ntok):
         np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
     for pool in pools:
         pool.close()
+
+
+def _run_slots(dtype, h_in, h_out, slot_ranks, req_slots, req_ntok, seed, n_slots, max_tokens=4096):
+    """_run_case with an explicit slot capacity (catalog-sized pools)."""
+    from paper_2411_17741_b200.ops import lora_apply
+
+    rng = np.random.default_rng(seed)
+    bf16 = dtype == torch.bfloat16
+    adapters = make_adapters(rng, slot_ranks, h_in, h_out, bf16=bf16)
+    T = int(np.sum(req_ntok))
+    x = rng.standard_normal((T, h_in)).astype(np.float32)
+    y0 = rng.standard_normal((T, h_out)).astype(np.float32)
+    if bf16:
+        x, y0 = bf16_round(x), bf16_round(y0)
+    npages = sum(-(-r // 8) for r in slot_ranks.values())
+    pool = _pool(1, [h_in], [h_out], dtype, npages, n_slots=n_slots, max_tokens=max_tokens)
+    _install(pool, {s: [adapters[s]] for s in slot_ranks}, slot_ranks, device_pack=True)
+    req_rank = [slot_ranks[s] if s >= 0 else 0 for s in req_slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(req_slots, req_rank, req_ntok)
+    xd = torch.from_numpy(x).to("cuda", dtype)
+    yd = torch.from_numpy(y0).to("cuda", dtype)
+    lora_apply(xd, yd, seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=0, perm=perm)
+    torch.cuda.synchronize()
+    got = yd.float().cpu().numpy()
+    ref = lora_apply_ref(x, y0, perm, seg_off, seg_slot, seg_rank, adapters)
+    pool.close()
+    return got, ref
+
+
+def test_c2_full_batch_one_layer_proj_bf16():
+    """C2 at full size for one (layer, proj): the seed-0 decode batch of 256 tokens over the
+    100-adapter catalog (82 distinct adapters, ranks 8-128), Llama-2-7B h=4096, bf16."""
+    from paper_2411_17741_b200.model import build_catalog
+    from paper_2411_17741_b200.workload import decode_batch
+
+    catalog = build_catalog(100)
+    ids = list(catalog)
+    slot_of = {a: i for i, a in enumerate(ids)}
+    slot_ranks = {i: catalog[a].rank for i, a in enumerate(ids)}
+    batch = decode_batch(0, 256, 100)
+    assert len(set(batch)) == 82
+    got, ref = _run_slots(torch.bfloat16, 4096, 4096, slot_ranks, [slot_of[a] for a in batch], [1] * 256,
+                          seed=41, n_slots=100)
+    np.testing.assert_allclose(got, ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_maximum_segments_and_tokens():
+    """The limits at once: 512 segments (kMaxSegments), 4096 tokens (max_tokens), ranks up to
+    128 (kMaxRank); 8-token requests stay on the decode kernel, fp32 rtol 1e-5."""
+    rng = np.random.default_rng(77)
+    ranks = [8, 16, 32, 64, 128, 24, 40, 120]
+    slot_ranks = {s: ranks[s % len(ranks)] for s in range(512)}
+    req_slots = rng.permutation(512).tolist()
+    got, ref = _run_slots(torch.float32, 256, 128, slot_ranks, req_slots, [8] * 512, seed=78, n_slots=512)
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-4)
