@@ -107,6 +107,7 @@ struct alignas(64) Params {
   float* v_out;            // MODE_SHRINK: v [position][v_stride]
   const float* v_in;       // MODE_EXPAND: v [position][v_stride]
   int v_stride;
+  int n_pages, n_tokens;   // pool pages, activation rows (bounds checks of CHAM_PF_CHECK builds)
   unsigned long long* trace;  // debug timeline [cta][unit k][8] (null = off)
   int trace_cap;
 };
@@ -437,6 +438,17 @@ constexpr bool kWarmL2 = CHAM_WARM_L2 != 0;
 #define CHAM_EXP_NOEPI 0  // experiment builds only: the expand epilogue skips the y update
 #endif
 constexpr bool kNoEpi = CHAM_EXP_NOEPI != 0;
+#ifndef CHAM_PF_CHECK
+#define CHAM_PF_CHECK 0  // debug builds: bounds-check every copy the loader issues, trap with a report
+#endif
+#define PF_CHECK(cond, code, a, b)                                                                          \
+  do {                                                                                                    \
+    if (CHAM_PF_CHECK && !(cond)) {                                                                       \
+      printf("PF_CHECK %d failed: cta %d warp %d lane %d a=%lld b=%lld\n", (code), (int)blockIdx.x,     \
+             (int)(threadIdx.x >> 5), (int)(threadIdx.x & 31), (long long)(a), (long long)(b));           \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
 // Warm L2 with a unit's operands as long contiguous runs (one x/y row range per token, one
 // run of atoms per adapter page): the TMA box loads then move 128-byte row pieces out of L2
 // instead of scattering 128-byte requests over DRAM pages.
@@ -677,6 +689,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (h * 64 < u.m) bytes += nch * (c64[h] ? 64 * 128 : min(64, u.m - h * 64) * 128);
+          PF_CHECK(bytes <= STAGE && u.kpc * u.xb + u.jps * np_pad * u.kpc * kAtomBytes <= STAGE, 1, bytes, u.kpc);
+          PF_CHECK(kc0 + c_first + nch <= p.h_in / 64 && nch > 0, 2, kc0 + c_first + nch, nch);
+          PF_CHECK(lane >= u.np || (my_page >= 0 && my_page < p.n_pages), 3, my_page, u.slot);
+          PF_CHECK(u.job0 + u.jps <= p.n_jobs && u.tile < tl.n_tiles, 4, u.job0, u.tile);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) PF_CHECK(b * 32 >= u.m || (rows[b] >= 0 && rows[b] < p.n_tokens), 5, rows[b], b);
           if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
           __syncwarp();
           unsigned char* stg = sm.ring[st];
@@ -718,6 +736,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             while (ld_acquire_gpu(p.tile_cnt + u.tile) < need) __nanosleep(32);
           asm volatile("fence.proxy.async.global;" ::: "memory");
           const uint32_t vbytes = u.ks * u.vstride;
+          PF_CHECK(vbytes <= VBUF && vbytes > 0 && u.tile < tl.n_tiles && u.job < p.n_jobs, 6, vbytes, u.tile);
           mbar_arrive_expect_tx(&sm.vfull[vb], vbytes);
           bulk_g2s(sm.vbuf[vb], vimg_of(p, u.job, u.tile), vbytes, &sm.vfull[vb], pol_w);
         }
@@ -748,6 +767,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (h * 64 < u.m) bytes += ng * (c64[h] ? 64 * 128 : min(64, u.m - h * 64) * 128);
+          PF_CHECK(bytes <= STAGE && u.kpc * u.bstride + ng * u.xb <= STAGE && ng > 0, 7, bytes, ng);
+          PF_CHECK(u.col0 / 64 + g_first + ng <= p.h_out / 64, 8, u.col0, g_first);
+          PF_CHECK(lane >= u.np || (my_page >= 0 && my_page < p.n_pages), 9, my_page, u.slot);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) PF_CHECK(b * 32 >= u.m || (rows[b] >= 0 && rows[b] < p.n_tokens), 10, rows[b], b);
           if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], bytes);
           __syncwarp();
           // B atoms [page][group]: one copy of the stage's ng groups per page
@@ -1084,6 +1108,8 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   Params prm{};
   prm.base = pool->base;
   prm.page_bytes = (long long)pool->page_bytes;
+  prm.n_pages = pool->n_pages;
+  prm.n_tokens = n_tokens;
   prm.slot_pages = pool->d_slot_pages;
   prm.h_in = pool->h_in[projs[0]];
   prm.h_out = pool->h_out[projs[0]];
