@@ -267,6 +267,7 @@ struct Shared {
   uint64_t plan_bar;
   int last_cta;  // this CTA re-arms the counters at exit
   int* pub_slot[PQ];
+  unsigned pub_bits[PQ];
   uint64_t pub_full[PQ], pub_empty[PQ];
   int unit_mailbox;
   Schedule sched;
@@ -575,11 +576,12 @@ __device__ __forceinline__ void trace_consumer(const Params& p, int seq, int fie
 // += 1) by a dedicated publisher warp: its gpu-scope fence waits for the stores to be
 // acknowledged, which would otherwise stall a consumer warp (and with it the stage release)
 // for a full store round trip on every unit.
-__device__ __forceinline__ void post_publish(Shared& sm, int& npub, int* ctr) {
+__device__ __forceinline__ void post_publish(Shared& sm, int& npub, int* ctr, unsigned bits = 0u) {
   const int k = npub++;
   const int slot = k % PQ;
   if (k >= PQ) mbar_wait(&sm.pub_empty[slot], ((k / PQ) - 1) & 1);
   sm.pub_slot[slot] = ctr;
+  sm.pub_bits[slot] = bits;
   mbar_arrive(&sm.pub_full[slot]);
 }
 
@@ -681,7 +683,7 @@ __device__ __forceinline__ void shrink_unit_mma(const Params& p, const Plan& pl,
     __syncwarp();
     if (lane == 0) {
       const int tile = pl.ex_start[pl.order_pos[m0.seg]] + (m0.pos0 - pl.seg_off[m0.seg]) / TG;
-      post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile);
+      post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile, 1u << m0.g);
     }
   }
 }
@@ -758,7 +760,7 @@ __device__ __forceinline__ void shrink_unit(const Params& p, const Plan& pl, K1S
     __syncwarp();
     if (lane == 0) {
       const int tile = pl.ex_start[pl.order_pos[m0.seg]] + (m0.pos0 - pl.seg_off[m0.seg]) / TG;
-      post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile);
+      post_publish(sm, npub, p.tile_ctr + m0.job * pl.totals[1] + tile, 1u << m0.g);
     }
   }
 }
@@ -1120,6 +1122,18 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
   return r;
 }
 
+#ifndef CHAM_PAGE_READY
+#define CHAM_PAGE_READY 0  // 1: tile counters as page bitmasks, an expand stage waits for its own pages only (C2 117.0k vs 117.3k)
+#endif
+constexpr bool kPageReady = CHAM_PAGE_READY != 0;
+// pages [pg0, pg0 + n) of a tile as a mask (np <= 32 pages per adapter)
+__device__ __forceinline__ unsigned page_bits(int pg0, int n) {
+  return (n >= 32 ? 0xffffffffu : ((1u << n) - 1u)) << pg0;
+}
+// all np shrink units of the tile published (counter or page mask)
+__device__ __forceinline__ bool tile_ready(int v, int np) {
+  return kPageReady ? ((unsigned)v & page_bits(0, np)) == page_bits(0, np) : v >= np;
+}
 #ifndef CHAM_EARLY_A
 #define CHAM_EARLY_A 0  // 1: A chunks of the whole first ring pass before griddepcontrol.wait (C2 114.0k vs 115.2k off)
 #endif
@@ -1330,7 +1344,17 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
     }
     if (y_here && lane < tcount)
       bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
-    if (fused && k == 0) {
+    if (fused && kPageReady) {
+      // this stage's v rows are final once the shrink units of ITS pages published (writers:
+      // v stores, proxy fence; publisher warp: gpu fence, page bit).  The mask was peeked when
+      // the unit was claimed and is refreshed only while a needed page is still in flight.
+      const unsigned need = page_bits(pg0, npg);
+      if (lane == 0 && ((unsigned)rdy & need) != need) {
+        const int* c = p.tile_ctr + job * NTL + tile;
+        while ((((unsigned)(rdy = ld_acquire_gpu(c))) & need) != need) __nanosleep(20);
+      }
+      __syncwarp();
+    } else if (fused && k == 0) {
       // the tile's v rows are complete once all np shrink units of (job, tile) published
       // (writers: v stores, proxy fence; publisher warp: gpu fence, counter).  The counter
       // was peeked when the unit was claimed; only a tile still in flight then is polled.
@@ -1412,7 +1436,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
   };
   auto np_of = [](const int4& a) { return (a.z >> 8) & 0xff; };
   while (unit >= 0 || has_def) {
-    if (has_def && (unit < 0 || __shfl_sync(0xffffffffu, def_rdy >= np_of(def_a), 0))) {
+    if (has_def && (unit < 0 || __shfl_sync(0xffffffffu, tile_ready(def_rdy, np_of(def_a)), 0))) {
       seq = issue_expand<T>(p, sm, seq, waited, pend, fused, def_up.job, def_up.cc, def_up.di, def_up.half, def_up.tier, def_a,
                             def_b, def_rdy, def_unit);
       has_def = false;
@@ -1425,7 +1449,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
     if (nunit >= 0) fetch(nunit, nup, na, nb, nrdy);
     if (up.kind == KIND_SHRINK) {
       seq = issue_shrink<T>(p, sm, seq, waited, pend, up.job, da, db);
-    } else if (kDefer && fused && !has_def && !__shfl_sync(0xffffffffu, rdy >= np_of(da), 0)) {
+    } else if (kDefer && fused && !has_def && !__shfl_sync(0xffffffffu, tile_ready(rdy, np_of(da)), 0)) {
       has_def = true;  // set aside; re-read below
       def_unit = unit;
       def_up = up;
@@ -1476,10 +1500,14 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
         const int slot = k % PQ;
         mbar_wait(&sm.pub_full[slot], (k / PQ) & 1);
         int* c = sm.pub_slot[slot];
+        const unsigned bits = sm.pub_bits[slot];
         mbar_arrive(&sm.pub_empty[slot]);
         if (!c) break;
         __threadfence();  // cumulative: the consumers' v stores (acquired through pub_full)
-        atomicAdd(c, 1);
+        if (kPageReady && bits)
+          atomicOr(reinterpret_cast<unsigned*>(c), bits);  // page g of the tile is final
+        else
+          atomicAdd(c, 1);  // tile counters without page masks; split-unit partials
       }
     }
   } else if (warp == GROUP_WARPS) {
