@@ -9,8 +9,9 @@ A step = the device segment-table build (K4) + LoRA apply for all 32 layers x 4 
 Synthetic random-init adapters (pool pages filled with N(0, 0.02) bf16) and activations.
 
 value    = tokens/s over all ranks, inputs resident in HBM (max over ranks of the CUDA-event time)
-e2e      = tokens/s through LoraStepExecutor with host buffers: pinned H2D of the request
-           table + the step's hidden state, the step's graph, D2H of the last projection's output
+e2e      = tokens/s through LoraStepExecutor with host buffers: every step's pinned H2D of the
+           request table + hidden state, the step's graph, D2H of the last projection's output;
+           wall clock over all steps, PCIe transfers overlapped with neighbouring steps
 roofline = algorithmic bytes of the apply launches / their measured duration vs
            MEASURED_PEAKS.json hbm_gbs
 cpu_baseline = the numpy oracle (oracle/lora_ref.py) on the host cores, bounded sample
