@@ -570,8 +570,10 @@ def run_c5(args, rank: int, world: int):
     decode batch of 256 tokens, tensor parallel over the N ranks (TP = N; every rank sees the
     same tokens).  A step = per layer: shrink of the rank's x shard for q/k/v into one fused
     [T, 3 x 64] fp32 v, ONE all-reduce of it, expand into the rank's y shards; then the same for
-    o (its own all-reduce): 160 all-reduces per step at N > 1 (tp.py).  The step is
-    one CUDA graph (NCCL all-reduces captured); value = tokens/s of the TP group."""
+    o (its own all-reduce): 160 all-reduces per step at N > 1 (tp.py).  At TP
+    degree 1 there is no exchange step and TensorParallelLora runs the fused apply instead (q,
+    k+v, o: 3 launches per layer).  The step is one CUDA graph (NCCL all-reduces captured);
+    value = tokens/s of the TP group."""
     import torch
     import torch.distributed as dist
 
@@ -682,10 +684,12 @@ def run_c5(args, rank: int, world: int):
             "adapter_read_gbs_per_rank": adapter_rank / (step_ms * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "kernel": "decode::lora_apply_kernel<bf16> MODE_SHRINK / MODE_EXPAND around the all-reduce "
-                                   "(rank 0's step incl. collectives)",
-                         "bytes_per_step_per_rank": bytes_rank, "launches_per_step": L70 * 8},
-            "gpu_launches": args.steps * L70 * 8,
+                         "kernel": ("decode::lora_apply_kernel<bf16> MODE_SHRINK / MODE_EXPAND around the all-reduce "
+                                    "(rank 0's step incl. collectives)") if world > 1 else
+                                   "decode::lora_apply_kernel<bf16> fused (TP degree 1: no exchange, q and k+v and o "
+                                   "launches)",
+                         "bytes_per_step_per_rank": bytes_rank, "launches_per_step": L70 * (5 if world > 1 else 3)},
+            "gpu_launches": args.steps * L70 * (5 if world > 1 else 3),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -164,6 +164,24 @@ def lora_apply_multi(xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], tab
          _stream_ptr(stream))
 
 
+def lora_apply_multi_arrays(xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], slot_ids, seg_offsets, ranks, *,
+                            pool: AdapterPool, layer: int, projs: Sequence[int], perm=None,
+                            n_seg: Optional[int] = None, plan=None, stream=None):
+    """lora_apply_multi over explicit segment arrays (projections sharing h_in and h_out)."""
+    if not (len(xs) == len(ys) == len(projs)):
+        raise ValueError("xs, ys and projs must have equal length")
+    for x, y, p in zip(xs, ys, projs):
+        _check_act(x, pool, pool.h_in[p], "x")
+        _check_act(y, pool, pool.h_out[p], "y")
+    ss, so, sr, pm = _tables(slot_ids, seg_offsets, ranks, perm, pool.device)
+    n = len(projs)
+    xa = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
+    ya = (ctypes.c_void_p * n)(*[y.data_ptr() for y in ys])
+    call("cham_lora_apply_multi", pool.handle, int(layer), n, _lib.int_array(projs), xa, ya, int(xs[0].shape[0]),
+         _lib.ptr(pm), so.data_ptr(), ss.data_ptr(), sr.data_ptr(), ss.numel() if n_seg is None else int(n_seg),
+         None, _lib.ptr(plan), _stream_ptr(stream))
+
+
 def _check_v(v: torch.Tensor) -> None:
     """v: fp32 [positions, cols] with unit column stride; the row stride (a multiple of 4
     floats, 16-byte aligned base) is passed as v_stride, so a column slice of a wider

@@ -81,6 +81,11 @@ class TensorParallelLora:
         self.v = torch.zeros(int(max_tokens) * width, dtype=torch.float32, device=dev)
         self.allreduce_count = 0
 
+    def _world(self) -> int:
+        if self.group is False or not dist.is_initialized():
+            return 1
+        return dist.get_world_size(self.group)
+
     def _check_ranks(self, seg_rank) -> None:
         if seg_rank is None or len(seg_rank) == 0:
             return
@@ -93,6 +98,19 @@ class TensorParallelLora:
                     plan=None, stream=None) -> None:
         """x: this rank's x shard [T, h_in/tp] (shared by projs); ys[i]: y shard of projs[i]."""
         T = x.shape[0]
+        if self.multi and self._world() == 1:
+            # TP degree 1: no exchange step, so the fused apply (shrink and expand in one
+            # launch per run of projections sharing h_out) replaces the two halves
+            i = 0
+            while i < len(projs):
+                j = i + 1
+                while j < len(projs) and self.pool.h_out[projs[j]] == self.pool.h_out[projs[i]]:
+                    j += 1
+                ops.lora_apply_multi_arrays([x] * (j - i), list(ys[i:j]), slot_ids, seg_offsets, ranks,
+                                            pool=self.pool, layer=layer, projs=list(projs[i:j]), perm=perm,
+                                            plan=plan, stream=stream)
+                i = j
+            return
         n_pos = T if n_positions is None else int(n_positions)
         R = self.r_stride
         v = self.v[: n_pos * len(projs) * R].view(n_pos, len(projs) * R)

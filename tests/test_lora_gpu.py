@@ -490,3 +490,31 @@ def test_maximum_segments_and_tokens():
     req_slots = rng.permutation(512).tolist()
     got, ref = _run_slots(torch.float32, 256, 128, slot_ranks, req_slots, [8] * 512, seed=78, n_slots=512)
     np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-4)
+
+
+def test_tensor_parallel_degree1_uses_fused_apply():
+    """TensorParallelLora at TP degree 1 (no exchange step) runs the fused apply per run of
+    projections sharing h_out (q alone, k+v together under GQA) and must equal the oracle."""
+    from paper_2411_17741_b200.tp import TensorParallelLora
+
+    rng = np.random.default_rng(19)
+    H_IN, H_OUT = [1024, 1024, 1024], [1024, 128, 128]
+    slot_ranks = {0: 64, 1: 16, 2: 8}
+    full = [make_adapters(rng, slot_ranks, H_IN[p], H_OUT[p], bf16=True) for p in range(3)]
+    req_slots = rng.integers(0, 3, 30).tolist()
+    req_rank = [slot_ranks[s] for s in req_slots]
+    perm, seg_off, seg_slot, seg_rank = build_segments_ref(req_slots, req_rank, [1] * 30)
+    x = bf16_round(rng.standard_normal((30, 1024)).astype(np.float32))
+    ys = [bf16_round(rng.standard_normal((30, H_OUT[p])).astype(np.float32)) for p in range(3)]
+    pool = _pool(1, H_IN, H_OUT, torch.bfloat16, 3 * 8, max_tokens=256)
+    _install(pool, {s: [full[p][s] for p in range(3)] for s in slot_ranks}, slot_ranks)
+    tp = TensorParallelLora(pool, max_tokens=256, r_stride=64, proj_groups=[[0, 1, 2]], group=False)
+    xd = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    yd = [torch.from_numpy(ys[p]).to("cuda", torch.bfloat16) for p in range(3)]
+    tp.apply_layer(0, [xd], yd, seg_slot, seg_off, seg_rank, perm=perm)
+    torch.cuda.synchronize()
+    assert tp.allreduce_count == 0
+    for p in range(3):
+        ref = lora_apply_ref(x, ys[p], perm, seg_off, seg_slot, seg_rank, full[p])
+        np.testing.assert_allclose(yd[p].float().cpu().numpy(), ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+    pool.close()
