@@ -1122,6 +1122,10 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
   return r;
 }
 
+#ifndef CHAM_PUB_FENCE
+#define CHAM_PUB_FENCE 1  // publisher: fence + relaxed atomic (1) or one release reduction (0)
+#endif
+constexpr bool kPubFence = CHAM_PUB_FENCE != 0;
 #ifndef CHAM_PAGE_READY
 #define CHAM_PAGE_READY 0  // 1: tile counters as page bitmasks, an expand stage waits for its own pages only (C2 117.0k vs 117.3k)
 #endif
@@ -1503,11 +1507,14 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
         const unsigned bits = sm.pub_bits[slot];
         mbar_arrive(&sm.pub_empty[slot]);
         if (!c) break;
-        __threadfence();  // cumulative: the consumers' v stores (acquired through pub_full)
+        if (kPubFence) __threadfence();  // explicit fence before the release (A/B switch)
         if (kPageReady && bits)
           atomicOr(reinterpret_cast<unsigned*>(c), bits);  // page g of the tile is final
-        else
+        else if (kPubFence)
           atomicAdd(c, 1);  // tile counters without page masks; split-unit partials
+        else
+          red_release_gpu_add(c, 1);  // release is cumulative over the consumers' v stores
+                                      // (acquired through pub_full)
       }
     }
   } else if (warp == GROUP_WARPS) {
