@@ -223,6 +223,50 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void trace_put(const Params& p, int k, int field, unsigned long long v) {
   if (p.trace && k < p.trace_cap) p.trace[((long long)blockIdx.x * p.trace_cap + k) * 8 + field] = v;
 }
+// debug breadcrumbs of the CTA's own progress (trace builds only): slot trace_cap - 1,
+// written by thread 0 and pushed to memory at system scope (the trace may be host-mapped)
+__device__ __forceinline__ void crumb(const Params& p, int field, unsigned long long v) {
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[((long long)blockIdx.x * p.trace_cap + p.trace_cap - 1) * 8 + field] = v;
+    __threadfence_system();
+  }
+}
+#ifndef CHAM_PF_DRAIN
+#define CHAM_PF_DRAIN 1  // drain the MMA warp's commit arrivals before the CTA exits
+#endif
+constexpr bool kDrain = CHAM_PF_DRAIN != 0;
+#ifndef CHAM_PF_WATCHDOG
+#define CHAM_PF_WATCHDOG 0  // debug builds: report mbarrier waits longer than 30 us into the trace
+#endif
+// Debug builds (CHAM_PF_WATCHDOG, trace on): a wait that is not satisfied after 30 us writes,
+// once per warp, the barrier's raw state and the waiter into trace slot cap-2-warp, then keeps
+// waiting.  Otherwise a plain mbarrier wait.
+__device__ __forceinline__ void pf_wait(const Params& p, uint64_t* bar, uint32_t parity, int tag, int a, int b) {
+  if (!CHAM_PF_WATCHDOG || !p.trace) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const unsigned long long t0 = gtimer();
+  bool rep = false;
+  while (!mbar_try_wait(bar, parity)) {
+    if (!rep && (threadIdx.x & 31) == 0 && gtimer() - t0 > 30000ull) {
+      rep = true;
+      unsigned long long raw;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(smem_u32(bar)) : "memory");
+      unsigned long long* d =
+          p.trace + ((long long)blockIdx.x * p.trace_cap + p.trace_cap - 2 - (threadIdx.x >> 5)) * 8;
+      d[1] = raw;
+      d[2] = parity;
+      d[3] = (unsigned long long)(smem_u32(bar));
+      d[4] = (unsigned long long)(unsigned)a;
+      d[5] = (unsigned long long)(unsigned)b;
+      d[6] = gtimer();
+      d[7] = (unsigned long long)p.epoch;
+      d[0] = (unsigned long long)(tag + 1);
+      __threadfence_system();
+    }
+  }
+}
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
 }
@@ -503,6 +547,7 @@ struct Shared {
   uint64_t full[NS], empty[NS];
   uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[2], tempty_ex[2];
   uint64_t vfull[2], vempty[2];
+  uint64_t drain;  // the MMA warp's last commit: every earlier commit arrival has landed
   uint64_t ufull[UQ], uempty[UQ];
   int uslot[UQ];
   uint32_t tmem_base;
@@ -543,13 +588,13 @@ __device__ __forceinline__ void write_v_chunk(char* img, const Unit& u, int r, i
 // Epilogue set -> its publisher warp.  The set's partial / V stores precede the post through
 // the set's named barrier (CTA-scope ordering) and the release of pq_full; the publisher's
 // gpu-scope fences are cumulative, so the epilogue warps never wait on a store round trip.
-__device__ __forceinline__ void post_event(Shared& sm, int es, int& npost, int tile, int kind, int et) {
+__device__ __forceinline__ void post_event(const Params& p, Shared& sm, int es, int& npost, int tile, int kind, int et) {
   asm volatile("fence.proxy.async.global;" ::: "memory");  // this thread's V stores -> TMA reads
   named_bar_sync(BAR_EPI + es, 128);
   if (et == 0) {
     const int k = npost;
     const int q = k % PQN;
-    if (k >= PQN) mbar_wait(&sm.pq_empty[es][q], ((k / PQN) - 1) & 1);
+    if (k >= PQN) pf_wait(p, &sm.pq_empty[es][q], ((k / PQN) - 1) & 1, 1, k, 0);
     sm.pq_tile[es][q] = tile;
     sm.pq_kind[es][q] = kind;
     mbar_arrive(&sm.pq_full[es][q]);
@@ -563,7 +608,7 @@ __device__ void publisher(const Params& p, Shared& sm, int es) {
   const int lane = threadIdx.x & 31;
   for (int k = 0;; ++k) {
     const int q = k % PQN;
-    mbar_wait(&sm.pq_full[es][q], (k / PQN) & 1);
+    pf_wait(p, &sm.pq_full[es][q], (k / PQN) & 1, 2, k, 0);
     const int tile = sm.pq_tile[es][q], kind = sm.pq_kind[es][q];
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.pq_empty[es][q]);
@@ -580,6 +625,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Shared& sm = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  crumb(p, 6, (unsigned long long)p.epoch);
+  crumb(p, 0, gtimer());
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&sm.full[i], 1);
@@ -593,6 +640,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       mbar_init(&sm.vfull[i], 1);
       mbar_init(&sm.vempty[i], 1);
     }
+    mbar_init(&sm.drain, 1);
     for (int i = 0; i < UQ; ++i) {
       mbar_init(&sm.ufull[i], 1);
       mbar_init(&sm.uempty[i], 1 + 8);
@@ -619,7 +667,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   tc_fence_after();
   const TileList& tl = sm.tl;
   const uint32_t tmem = sm.tmem_base;
+  crumb(p, 1, gtimer());
   pdl_wait();  // x, y, v and the workspaces may belong to the previous kernel
+  crumb(p, 2, gtimer());
   pdl_launch_dependents();
   if (!sm.flag) {
     if (tid == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
@@ -651,7 +701,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       // publish the unit id to the MMA and epilogue warps
       const int q = k % UQ;
       if (lane == 0) {
-        if (k >= UQ) mbar_wait(&sm.uempty[q], ((k / UQ) - 1) & 1);
+        if (k >= UQ) pf_wait(p, &sm.uempty[q], ((k / UQ) - 1) & 1, 3, k, 0);
         sm.uslot[q] = u_id;
         mbar_arrive(&sm.ufull[q]);
       }
@@ -683,7 +733,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int st = seq % NS;
           const int c_first = s * u.kpc;
           const int nch = min(u.kpc, u.nchunks - c_first);
-          if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
+          if (seq >= NS) pf_wait(p, &sm.empty[st], ((seq / NS) - 1) & 1, 4, seq, u_id);
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
           uint32_t bytes = nch * u.jps * u.np * kAtomBytes;
 #pragma unroll
@@ -729,7 +779,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         // ---- expand: V image of (job, tile), then B slices + y rows per 64-column group
         const int vb = nex & 1;
         if (lane == 0) {
-          if (nex >= 2) mbar_wait(&sm.vempty[vb], ((nex >> 1) - 1) & 1);
+          if (nex >= 2) pf_wait(p, &sm.vempty[vb], ((nex >> 1) - 1) & 1, 5, nex, u_id);
           // every phase-1 unit of the tile has published its partial V image
           const int need = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
           if (cur_flag < need)
@@ -753,7 +803,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int st = seq % NS;
           const int g_first = s * u.kpc;
           const int ng = min(u.kpc, u.ngrp - g_first);
-          if (seq >= NS) mbar_wait(&sm.empty[st], ((seq / NS) - 1) & 1);
+          if (seq >= NS) pf_wait(p, &sm.empty[st], ((seq / NS) - 1) & 1, 6, seq, u_id);
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
           unsigned char* stg = sm.ring[st];
           if (pad) {
@@ -809,7 +859,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     for (int k = 0;; ++k) {
       if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 3, gtimer());
       const int q = k % UQ;
-      mbar_wait(&sm.ufull[q], (k / UQ) & 1);
+      pf_wait(p, &sm.ufull[q], (k / UQ) & 1, 7, k, 0);
       const int u_id = sm.uslot[q];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
@@ -818,7 +868,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       if (u.kind == 3) continue;
       if (u.kind == 1) {
         const int ab = nsh & 1;
-        if (nsh >= 2) mbar_wait(&sm.tempty_sh[ab], ((nsh >> 1) - 1) & 1);
+        if (nsh >= 2) pf_wait(p, &sm.tempty_sh[ab], ((nsh >> 1) - 1) & 1, 8, nsh, u_id);
         tc_fence_after();
         // (one MMA of N = jps * rp for the whole group would read x once per K step, but it
         // faulted intermittently in long PDL chains: one MMA per job)
@@ -826,7 +876,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
           const int nch = min(u.kpc, u.nchunks - s * u.kpc);
-          mbar_wait(&sm.full[st], (seq / NS) & 1);
+          pf_wait(p, &sm.full[st], (seq / NS) & 1, 9, seq, u_id);
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
           tc_fence_after();
           if (lane == 0) {
@@ -852,19 +902,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         ++nsh;
       } else {
         const int vb = nex & 1;
-        mbar_wait(&sm.vfull[vb], (nex >> 1) & 1);
+        pf_wait(p, &sm.vfull[vb], (nex >> 1) & 1, 10, nex, u_id);
         tc_fence_after();
         const uint32_t va = smem_u32(sm.vbuf[vb]);
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
           const int ng = min(u.kpc, u.ngrp - s * u.kpc);
-          mbar_wait(&sm.full[st], (seq / NS) & 1);
+          pf_wait(p, &sm.full[st], (seq / NS) & 1, 11, seq, u_id);
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
           tc_fence_after();
           const uint32_t base = smem_u32(sm.ring[st]);
           for (int g = 0; g < ng; ++g, ++ngrp) {
             const int acc = ngrp & 1;
-            if (ngrp >= 2) mbar_wait(&sm.tempty_ex[acc], ((ngrp >> 1) - 1) & 1);
+            if (ngrp >= 2) pf_wait(p, &sm.tempty_ex[acc], ((ngrp >> 1) - 1) & 1, 12, ngrp, u_id);
             tc_fence_after();
             if (lane == 0) {
               const uint32_t ba = base + g * kAtomBytes;  // B atoms [page][group]
@@ -900,12 +950,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     for (int k = 0;; ++k) {
       if (k > 0 && tid == 0 && p.trace) trace_put(p, k - 1, 5, gtimer());
       const int q = k % UQ;
-      mbar_wait(&sm.ufull[q], (k / UQ) & 1);
+      pf_wait(p, &sm.ufull[q], (k / UQ) & 1, 13, k, 0);
       const int u_id = sm.uslot[q];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
       if (u_id < 0) {
-        post_event(sm, es, npost, 0, 0, r);  // the publisher exits
+        post_event(p, sm, es, npost, 0, 0, r);  // the publisher exits
         break;
       }
       const Unit u = make_unit(p, tl, u_id);
@@ -923,7 +973,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             write_v_chunk(vimg_of(p, 0, u.tile), u, r, c0, v, nv);
           }
         }
-        post_event(sm, es, npost, u.tile, 2, r);
+        post_event(p, sm, es, npost, u.tile, 2, r);
         continue;
       }
       if (u.kind == 1) {
@@ -934,7 +984,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           ++nsh;
           continue;
         }
-        mbar_wait(&sm.tfull_sh[ab], (nsh >> 1) & 1);
+        pf_wait(p, &sm.tfull_sh[ab], (nsh >> 1) & 1, 14, nsh, u_id);
         if (r == 0 && p.trace) trace_put(p, k, 4, gtimer());
         tc_fence_after();
         ++nsh;
@@ -961,7 +1011,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty_sh[ab]);
         if (p.mode == MODE_SHRINK) continue;
-        post_event(sm, es, npost, u.tile, 2, r);
+        post_event(p, sm, es, npost, u.tile, 2, r);
         continue;
       }
       // ---- expand: y rows += D2 per 64-column group.  Each thread adds its row in place in
@@ -973,13 +1023,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       for (int s = 0; s < u.nst; ++s, ++seq) {
         const int st = seq % NS;
         const int ng = min(u.kpc, u.ngrp - s * u.kpc);
-        mbar_wait(&sm.full[st], (seq / NS) & 1);  // the y rows of this stage have landed
+        pf_wait(p, &sm.full[st], (seq / NS) & 1, 15, seq, u_id);  // the y rows of this stage have landed
         if (s == 0 && tid == 0 && p.trace) trace_put(p, k, 4, gtimer());
         const unsigned char* ybase = sm.ring[st] + u.kpc * u.bstride;
         for (int g = 0; g < ng; ++g, ++ngrp) {
           const int acc = ngrp & 1;
           if (acc != es) continue;  // the other set's group
-          mbar_wait(&sm.tfull_ex[acc], (ngrp >> 1) & 1);
+          pf_wait(p, &sm.tfull_ex[acc], (ngrp >> 1) & 1, 16, ngrp, u_id);
           tc_fence_after();
           float d0[32], d1[32];
           const uint32_t ta = tmem + TM_EX + acc * 64 + lane_off;
@@ -1025,7 +1075,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     }
   }
   // the last CTA re-arms this parity's counters
+  crumb(p, 3, gtimer());
+  if (kDrain && warp == W_MMA) {
+    // tcgen05.commit arrivals are asynchronous: a CTA that exits with one in flight lets it
+    // land in the shared memory of the next CTA on this SM (PDL starts it right away), on
+    // that CTA's freshly initialised barriers.  One more commit, waited for, drains them.
+    if (lane == 0) mma_commit(&sm.drain);
+    __syncwarp();
+    mbar_wait(&sm.drain, 0);
+  }
   __syncthreads();
+  crumb(p, 4, gtimer());
   if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem);
@@ -1043,6 +1103,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     }
     __threadfence();
   }
+  crumb(p, 5, gtimer());
 }
 
 }  // namespace prefill
