@@ -676,7 +676,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   } else if (warp == W_LOAD) {
     // ---------------------------------------------------------------- loader + dispatch
     const uint64_t pol_w = policy_evict_first();  // adapter pages: streamed
-    const uint64_t pol_x = policy_evict_last();   // x: re-read by the other job groups / K ranges
+#ifndef CHAM_PF_XPOL_NORMAL
+#define CHAM_PF_XPOL_NORMAL 0
+#endif
+    const uint64_t pol_x = CHAM_PF_XPOL_NORMAL ? policy_evict_normal() : policy_evict_last();  // x: re-read by the other job groups / K ranges
     const uint64_t pol_y = policy_evict_first();
     int next = blockIdx.x;  // first unit static, the rest from the counter (one claim ahead)
     int claim = 0;
