@@ -242,7 +242,8 @@ constexpr bool kDrain = CHAM_PF_DRAIN != 0;
 // once per warp, the barrier's raw state and the waiter into trace slot cap-2-warp, then keeps
 // waiting.  Otherwise a plain mbarrier wait.
 __device__ __forceinline__ void pf_wait(const Params& p, uint64_t* bar, uint32_t parity, int tag, int a, int b) {
-  if (!CHAM_PF_WATCHDOG || !p.trace) {
+  // CHAM_PF_WATCHDOG 2: watch only the stage-full waits (tags 9, 11, 15), the others plain
+  if (!CHAM_PF_WATCHDOG || !p.trace || (CHAM_PF_WATCHDOG == 2 && tag != 9 && tag != 11 && tag != 15)) {
     mbar_wait(bar, parity);
     return;
   }
