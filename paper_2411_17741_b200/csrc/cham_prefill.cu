@@ -231,6 +231,9 @@ __device__ __forceinline__ void crumb(const Params& p, int field, unsigned long 
     __threadfence_system();
   }
 }
+#ifndef CHAM_PF_LATE_ALLOC
+#define CHAM_PF_LATE_ALLOC 0  // 1: tcgen05.alloc after griddepcontrol.wait (fault-hunt experiment)
+#endif
 #ifndef CHAM_PF_DRAIN
 #define CHAM_PF_DRAIN 1  // drain the MMA warp's commit arrivals before the CTA exits
 #endif
@@ -660,6 +663,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     prefetch_map(&p.maps[lane].y1);
   }
   if (warp == W_MMA) {
+    // CHAM_PF_LATE_ALLOC: take the tensor memory only once the previous kernel has completed
+    if (CHAM_PF_LATE_ALLOC) pdl_wait();
     tmem_alloc(&sm.tmem_base);
     tc_fence_before();
   }
