@@ -231,6 +231,9 @@ __device__ __forceinline__ void crumb(const Params& p, int field, unsigned long 
     __threadfence_system();
   }
 }
+#ifndef CHAM_PF_MMA_SYNC
+#define CHAM_PF_MMA_SYNC 0  // 1: the MMA warp waits for each shrink stage's MMAs (fault-hunt experiment)
+#endif
 #ifndef CHAM_PF_LATE_ALLOC
 #define CHAM_PF_LATE_ALLOC 0  // 1: tcgen05.alloc after griddepcontrol.wait (fault-hunt experiment)
 #endif
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     publisher(p, sm, warp - W_PUB);
   } else if (warp == W_MMA) {
     // ---------------------------------------------------------------- MMA issuer
-    int seq = 0, nsh = 0, nex = 0, ngrp = 0;
+    int seq = 0, nsh = 0, nex = 0, ngrp = 0, ndrain = 0;
     const uint32_t idesc_ex = idesc_bf16(BM, 64, true);
     for (int k = 0;; ++k) {
       if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 3, gtimer());
@@ -872,7 +875,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       const int u_id = sm.uslot[q];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
-      if (u_id < 0) break;
+      if (u_id < 0) {
+        if (lane == 0) sm.last[1] = ndrain;  // drain phases used (CHAM_PF_MMA_SYNC)
+        __syncwarp();
+        break;
+      }
       const Unit u = make_unit(p, tl, u_id);
       if (u.kind == 3) continue;
       if (u.kind == 1) {
@@ -905,7 +912,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             mma_commit(&sm.empty[st]);
             mbar_arrive_cnt(&sm.empty[st], 8);  // the epilogue warps never read shrink stages
             if (s == u.nst - 1) mma_commit(&sm.tfull_sh[ab]);
+            if (CHAM_PF_MMA_SYNC) {  // fault-hunt experiment: one stage of MMAs in flight at a time
+              mma_commit(&sm.drain);
+              mbar_wait(&sm.drain, ndrain & 1);
+            }
           }
+          ++ndrain;
           __syncwarp();
         }
         ++nsh;
@@ -1091,7 +1103,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     // that CTA's freshly initialised barriers.  One more commit, waited for, drains them.
     if (lane == 0) mma_commit(&sm.drain);
     __syncwarp();
-    mbar_wait(&sm.drain, 0);
+    mbar_wait(&sm.drain, CHAM_PF_MMA_SYNC ? (sm.last[1] & 1) : 0);
   }
   __syncthreads();
   crumb(p, 4, gtimer());
