@@ -241,6 +241,9 @@ __device__ __forceinline__ void crumb(const Params& p, int field, unsigned long 
 #define CHAM_PF_DRAIN 1  // drain the MMA warp's commit arrivals before the CTA exits
 #endif
 constexpr bool kDrain = CHAM_PF_DRAIN != 0;
+// debug breadcrumb of the MMA warp's progress inside a shrink unit (trace builds with
+// CHAM_PF_WATCHDOG): slot trace_cap - 15 = {unit k, stage, seq, state, time}
+__device__ __forceinline__ void mma_mark(const Params& p, int k, int s, int seq, int state);
 #ifndef CHAM_PF_WATCHDOG
 #define CHAM_PF_WATCHDOG 0  // debug builds: report mbarrier waits longer than 30 us into the trace
 #endif
@@ -272,6 +275,18 @@ __device__ __forceinline__ void pf_wait(const Params& p, uint64_t* bar, uint32_t
       d[0] = (unsigned long long)(tag + 1);
       __threadfence_system();
     }
+  }
+}
+__device__ __forceinline__ void mma_mark(const Params& p, int k, int s, int seq, int state) {
+  if (CHAM_PF_WATCHDOG && p.trace && (threadIdx.x & 31) == 0) {
+    unsigned long long* d = p.trace + ((long long)blockIdx.x * p.trace_cap + p.trace_cap - 15) * 8;
+    d[0] = k;
+    d[1] = s;
+    d[2] = seq;
+    d[3] = state;
+    d[4] = gtimer();
+    d[5] = p.epoch;
+    __threadfence_system();
   }
 }
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
@@ -892,7 +907,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
           const int nch = min(u.kpc, u.nchunks - s * u.kpc);
+          mma_mark(p, k, s, seq, 1);  // waiting for the stage
           pf_wait(p, &sm.full[st], (seq / NS) & 1, 9, seq, u_id);
+          mma_mark(p, k, s, seq, 2);  // issuing
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
           tc_fence_after();
           if (lane == 0) {
@@ -912,6 +929,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             mma_commit(&sm.empty[st]);
             mbar_arrive_cnt(&sm.empty[st], 8);  // the epilogue warps never read shrink stages
             if (s == u.nst - 1) mma_commit(&sm.tfull_sh[ab]);
+            mma_mark(p, k, s, seq, 3);  // issued + committed
             if (CHAM_PF_MMA_SYNC) {  // fault-hunt experiment: one stage of MMAs in flight at a time
               mma_commit(&sm.drain);
               mbar_wait(&sm.drain, ndrain & 1);
