@@ -908,7 +908,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int st = seq % NS;
           const int nch = min(u.kpc, u.nchunks - s * u.kpc);
           mma_mark(p, k, s, seq, 1);  // waiting for the stage
+          if (lane == 0 && p.trace) trace_put(p, k, 3, (1ull << 62) | ((unsigned long long)s << 8) | 1);
           pf_wait(p, &sm.full[st], (seq / NS) & 1, 9, seq, u_id);
+          if (lane == 0 && p.trace) trace_put(p, k, 3, (1ull << 62) | ((unsigned long long)s << 8) | 2);
           mma_mark(p, k, s, seq, 2);  // issuing
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 2, gtimer());
           tc_fence_after();
@@ -930,6 +932,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             mbar_arrive_cnt(&sm.empty[st], 8);  // the epilogue warps never read shrink stages
             if (s == u.nst - 1) mma_commit(&sm.tfull_sh[ab]);
             mma_mark(p, k, s, seq, 3);  // issued + committed
+            if (p.trace) trace_put(p, k, 3, (1ull << 62) | ((unsigned long long)s << 8) | 3);
             if (CHAM_PF_MMA_SYNC) {  // fault-hunt experiment: one stage of MMAs in flight at a time
               mma_commit(&sm.drain);
               mbar_wait(&sm.drain, ndrain & 1);

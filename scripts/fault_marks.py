@@ -21,6 +21,10 @@ for i in sys.argv[1:]:
             r = tr[b, k]
             if r[0] >= tw and r[0] > 0 and not r[5] >= tw:
                 kind = int(r[6] >> 32)
+                f3 = int(r[3])
+                if f3 >> 62 == 1:
+                    print(f"    in-unit MMA progress: stage {(f3 >> 8) & 0xffffff} state {f3 & 0xff} "
+                          "(1 waiting for full, 2 issuing, 3 issued+committed)")
                 m = marks[b]
                 print(f"  cta {b} k {k} kind {kind} unit {int(r[6] & 0xffffffff)}; last MMA mark: ep {int(m[5])} "
                       f"unit k {int(m[0])} stage {int(m[1])} seq {int(m[2])} state {int(m[3])} "
