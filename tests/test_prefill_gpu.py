@@ -189,6 +189,16 @@ def test_random_mixed_batches_fuzz(seed):
     """Seeded random batches across both kernels: 1-48 requests of 1-150 tokens (segments of
     64+ tokens go to the tcgen05 kernel, the rest to the decode kernel), ranks 8-128 including
     non-multiples of 16, rectangular h_in/h_out, requests without an adapter."""
+    _fuzz(seed, torch.bfloat16)
+
+
+@pytest.mark.parametrize("seed", [201, 202, 203])
+def test_random_batches_fuzz_fp32(seed):
+    """The same random batches on an fp32 pool (decode kernel only), rtol 1e-5."""
+    _fuzz(seed, torch.float32)
+
+
+def _fuzz(seed, dtype):
     from oracle.lora_ref import bf16_round, lora_apply_ref, make_adapters
     from oracle.segments_ref import build_segments_ref
     from paper_2411_17741_b200.ops import lora_apply
@@ -198,7 +208,8 @@ def test_random_mixed_batches_fuzz(seed):
     h_in, h_out = int(rng.choice([256, 512, 1024])), int(rng.choice([256, 512, 1024]))
     n_slots = int(rng.integers(1, 9))
     slot_ranks = {s: int(rng.choice([8, 16, 24, 32, 40, 64, 72, 128])) for s in range(n_slots)}
-    adapters = make_adapters(rng, slot_ranks, h_in, h_out, bf16=True)
+    bf16 = dtype == torch.bfloat16
+    adapters = make_adapters(rng, slot_ranks, h_in, h_out, bf16=bf16)
     n_req = int(rng.integers(1, 49))
     req_slots = [int(s) if rng.random() > 0.1 else -1 for s in rng.integers(0, n_slots, n_req)]
     req_ntok = [int(rng.choice([1, 1, 2, 3, 64, 70, 100, 150])) for _ in range(n_req)]
@@ -208,9 +219,11 @@ def test_random_mixed_batches_fuzz(seed):
     req_rank = [slot_ranks[s] if s >= 0 else 0 for s in req_slots]
     perm, seg_off, seg_slot, seg_rank = build_segments_ref(req_slots, req_rank, req_ntok)
     T = int(sum(req_ntok))
-    x = bf16_round(rng.standard_normal((T, h_in)).astype(np.float32))
-    y0 = bf16_round(rng.standard_normal((T, h_out)).astype(np.float32))
-    pool = AdapterPool(sum(-(-r // 8) for r in slot_ranks.values()), 1, [h_in], [h_out], dtype=torch.bfloat16,
+    x = rng.standard_normal((T, h_in)).astype(np.float32)
+    y0 = rng.standard_normal((T, h_out)).astype(np.float32)
+    if bf16:
+        x, y0 = bf16_round(x), bf16_round(y0)
+    pool = AdapterPool(sum(-(-r // 8) for r in slot_ranks.values()), 1, [h_in], [h_out], dtype=dtype,
                        n_slots=n_slots, max_tokens=4096)
     page = 0
     for s, r in slot_ranks.items():
@@ -220,10 +233,11 @@ def test_random_mixed_batches_fuzz(seed):
         a, b = adapters[s]
         pool.fill_async(s, pool.pack_host([torch.from_numpy(a)], [torch.from_numpy(b)], r))
     torch.cuda.synchronize()
-    xd = torch.from_numpy(x).to("cuda", torch.bfloat16)
-    yd = torch.from_numpy(y0).to("cuda", torch.bfloat16)
+    xd = torch.from_numpy(x).to("cuda", dtype)
+    yd = torch.from_numpy(y0).to("cuda", dtype)
     lora_apply(xd, yd, seg_slot, seg_off, seg_rank, pool=pool, layer=0, proj=0, perm=perm)
     torch.cuda.synchronize()
     ref = lora_apply_ref(x, y0, perm, seg_off, seg_slot, seg_rank, adapters)
-    np.testing.assert_allclose(yd.float().cpu().numpy(), ref, rtol=2e-2, atol=2e-2)
+    tol = 2e-2 if bf16 else 1e-5
+    np.testing.assert_allclose(yd.float().cpu().numpy(), ref, rtol=tol, atol=tol if bf16 else 1e-4)
     pool.close()
