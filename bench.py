@@ -43,12 +43,30 @@ T_DECODE = 256
 NUM_ADAPTERS = 100
 
 
+WORKLOAD_C2 = ("C2: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers), 100 adapters ranks 8-128, "
+               "decode batch 256 tokens per GPU (assign_adapter seed = rank)")
+WORKLOAD_C3 = ("C3: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers) prefill, 64 segments x 64 tokens over "
+               "64 adapters with power-law ranks (prefill_batch seed = rank), tcgen05 path")
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1681.7)), "measured"
     return 6650.0, 1590.0, "fallback"
+
+
+def step_bytes(seg_off, seg_slot, seg_rank, n_tokens, h, es, n_layers, groups):
+    """Algorithmic bytes of one step, counting x ONCE per launch group: every
+    distinct adapter's A and B once per (layer, proj), y read + written once per (layer, proj),
+    and x read once per (layer, projection group) — a fused q/k/v launch stages the shared
+    input once for its three projections.  Returns (total, adapter part)."""
+    a_lp, _ = algorithmic_bytes(seg_off, seg_slot, seg_rank, n_tokens, h, h, es)
+    n_proj = sum(len(g) for g in groups)
+    adapter = a_lp * n_proj * n_layers
+    act = n_layers * (len(groups) * n_tokens * h * es + n_proj * 2 * n_tokens * h * es)
+    return adapter + act, adapter
 
 
 def algorithmic_bytes(seg_off, seg_slot, seg_rank, n_tokens, h_in, h_out, es):
@@ -88,7 +106,7 @@ class ClockSampler:
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
@@ -155,30 +173,80 @@ def cpu_oracle_sample(batch_ids, seconds: float = 12.0, ntok=None):
                        "numpy fp32")
 
 
+def cpu_full_step(batch_ids, n_steps: int, n_warm: int = 1, weight_sets: int = 4):
+    """The numpy fp32 restatement (oracle/lora_ref.py) of FULL steps: every (layer, proj) of the
+    32 x 4 applies of the batch, each over its own adapter weights drawn from `weight_sets`
+    rotating sets (4 x ~120 MB of distinct fp32 A/B, far beyond the host caches).  Returns
+    (per-step seconds list, cores, sample description)."""
+    from oracle.lora_ref import lora_apply_ref
+    from oracle.segments_ref import build_segments_ref
+    from paper_2411_17741_b200.workload import rank_of_id
+
+    rng = np.random.default_rng(0)
+    uniq = sorted(set(batch_ids))
+    slot = {a: i for i, a in enumerate(uniq)}
+    sets = []
+    for _ in range(weight_sets):
+        ad = {}
+        for a in uniq:
+            r = rank_of_id(a)
+            ad[slot[a]] = ((rng.standard_normal((H, r)) * 0.02).astype(np.float32),
+                           (rng.standard_normal((r, H)) * 0.02).astype(np.float32))
+        sets.append(ad)
+    ranks = [rank_of_id(a) for a in batch_ids]
+    slots = [slot[a] for a in batch_ids]
+    perm, off, sl, rk = build_segments_ref(slots, ranks, [1] * len(batch_ids))
+    x = rng.standard_normal((len(batch_ids), H)).astype(np.float32)
+    y = rng.standard_normal((len(batch_ids), H)).astype(np.float32)
+    times = []
+    for i in range(n_warm + n_steps):
+        t0 = time.perf_counter()
+        for lp in range(N_LAYERS * N_PROJ):
+            lora_apply_ref(x, y, perm, off, sl, rk, sets[lp % weight_sets], acc=np.float32)
+        if i >= n_warm:
+            times.append(time.perf_counter() - t0)
+    cores = len(os.sched_getaffinity(0))
+    return times, cores, (f"full steps: 128 (layer,proj) applies of the batch ({len(batch_ids)} tok, {len(uniq)} "
+                          f"adapters) over {weight_sets} rotating distinct weight sets, numpy fp32 (BLAS threads = "
+                          f"{cores} cores)")
+
+
+def decision_path_record():
+    try:
+        from bench_decisions import decision_path
+
+        return decision_path()
+    except Exception as e:  # the GPU line must not die on the CPU side-measurement
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
 def run_reference(args, rank: int, world: int):
+    """The reference arm: the reference has no LoRA implementation of its own (it models the
+    cost, engine.py:67-77), so its CPU path is the oracle port, timed over full C2 steps on all
+    host cores; the reference's own decision path (baseline/_ref) is timed beside it."""
     if rank != 0:
         return
+    from bench_decisions import cpu_model
     from paper_2411_17741_b200.workload import decode_batch
 
     batch = decode_batch(0, T_DECODE, NUM_ADAPTERS)
-    per_step = []
-    t_lp = None
-    for _ in range(args.warmup):
-        t_lp, cores, sample = cpu_oracle_sample(batch, seconds=0.5)
-    for _ in range(args.steps):
-        t_lp, cores, sample = cpu_oracle_sample(batch, seconds=max(1.0, 20.0 / max(args.steps, 1)))
-        per_step.append(t_lp * N_LAYERS * N_PROJ)
-    step_s = statistics.median(per_step)
+    n = max(1, min(args.steps, args.cpu_max_steps))
+    times, cores, sample = cpu_full_step(batch, n, n_warm=1 if args.warmup > 0 else 0)
+    step_s = statistics.median(times)
     value = T_DECODE / step_s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "steps": n, "warmup": 1 if args.warmup > 0 else 0, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2: Llama-2-7B q/k/v/o LoRA, 100 adapters ranks 8-128, decode batch 256 tokens",
-                   "global_batch": T_DECODE, "seq_len": 1, "parallelism": "replicas", "l2": "n/a (CPU)"},
+        "config": {"workload": WORKLOAD_C2, "global_batch": T_DECODE * world, "seq_len": 1,
+                   "parallelism": f"replicas x{world}", "launch_mode": args.mode,
+                   "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": sample + f"; step = 128 x that, per-step time = median of {args.steps}"},
+                         "cpu_model": cpu_model(),
+                         "sample": sample + f"; median of {n} timed full steps (--steps {args.steps} capped at "
+                                            f"--cpu-max-steps {args.cpu_max_steps})"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "decision_path": decision_path_record(),
     }
     print(json.dumps(line), flush=True)
 
@@ -269,25 +337,27 @@ def run_ours(args, rank: int, world: int):
     barrier()
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
-        with torch.cuda.stream(s):
-            ev0.record(s)
-            for _ in range(args.steps):
-                g_step.replay()
-            ev1.record(s)
-        torch.cuda.synchronize(dev)
-        barrier()
-        torch.cuda.synchronize(dev)
-        step_ms = ev0.elapsed_time(ev1) / args.steps
-        # apply-only graph for the roofline (the decode kernel launches alone)
-        reps = max(3, args.steps)
-        with torch.cuda.stream(s):
-            ev0.record(s)
-            for _ in range(reps):
-                g_apply.replay()
-            ev1.record(s)
-        torch.cuda.synchronize(dev)
-        apply_ms = ev0.elapsed_time(ev1) / reps
+    # clocks are sampled (every 20 ms) over the whole GPU measurement: the timed steps, the
+    # apply-only replays and the e2e loop
+    clk = ClockSampler(dev.index).__enter__()
+    with torch.cuda.stream(s):
+        ev0.record(s)
+        for _ in range(args.steps):
+            g_step.replay()
+        ev1.record(s)
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    # apply-only graph for the roofline (the decode kernel launches alone)
+    reps = max(3, args.steps)
+    with torch.cuda.stream(s):
+        ev0.record(s)
+        for _ in range(reps):
+            g_apply.replay()
+        ev1.record(s)
+    torch.cuda.synchronize(dev)
+    apply_ms = ev0.elapsed_time(ev1) / reps
     step_ms = max_over_ranks(step_ms)
     apply_ms_max = max_over_ranks(apply_ms)
 
@@ -351,14 +421,13 @@ def run_ours(args, rank: int, world: int):
     s.synchronize()
     cs.synchronize()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    clk.__exit__()
 
     # ---- algorithmic bytes / flops from the rank's segment table
     perm, off, sl, rk = ex.table.to_host()
-    a_bytes, act_bytes = algorithmic_bytes(off, sl, rk, T, H, H, 2)
-    a_bytes, act_bytes = int(a_bytes), int(act_bytes)
     lp = N_LAYERS * N_PROJ
-    bytes_step = (a_bytes + act_bytes) * lp
-    adapter_bytes_step = a_bytes * lp
+    bytes_step, adapter_bytes_step = step_bytes(off, sl, rk, T, H, 2, N_LAYERS, groups)
+    bytes_step, adapter_bytes_step = int(bytes_step), int(adapter_bytes_step)
     flops_step = int(2 * sum(int(rk[i]) * int(off[i + 1] - off[i]) for i in range(len(sl))) * (H + H) * lp)
     hbm_peak, bf16_peak, peak_kind = peaks()
     apply_launches = N_LAYERS * len(groups)
@@ -368,12 +437,10 @@ def run_ours(args, rank: int, world: int):
         tokens_total = T * world
         value = tokens_total / (step_ms * 1e-3)
         if args.config == "c3":
-            workload = ("C3: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers) prefill, 64 segments x 64 tokens over "
-                        "64 adapters with power-law ranks (prefill_batch seed = rank), tcgen05 path")
+            workload = WORKLOAD_C3
             kernels = "prefill::fused_kernel (tcgen05, TMEM accumulators; shrink -> per-tile V images -> expand, PDL-chained) per apply"
         else:
-            workload = ("C2: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers), 100 adapters ranks 8-128, "
-                        "decode batch 256 tokens per GPU (assign_adapter seed = rank)")
+            workload = WORKLOAD_C2
             kernels = "decode::lora_apply_kernel<bf16> (shrink and expand units from one queue, per-tile v-ready counters, PDL-chained)"
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -389,7 +456,10 @@ def run_ours(args, rank: int, world: int):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "kernel": kernels,
-                         "bytes_per_step": bytes_step, "launches_per_step": apply_launches,
+                         "bytes_per_step": bytes_step,
+                         "bytes_formula": "SURVEY 8(d) per (layer, proj): distinct adapters' A+B once, y read+write; "
+                                          "x once per launch group (q/k/v share one staged input)",
+                         "launches_per_step": apply_launches,
                          "algorithmic_bytes_per_launch": bytes_step / apply_launches,
                          "avg_launch_us": apply_ms * 1e3 / apply_launches,
                          "traffic": traffic_per_launch(args.config),
@@ -406,9 +476,14 @@ def run_ours(args, rank: int, world: int):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
+            from bench_decisions import cpu_model
+
             t_lp, cores, sample = cpu_oracle_sample(batch, seconds=args.cpu_seconds, ntok=list(req_ntok))
             line["cpu_baseline"] = {"value": T / (t_lp * lp), "unit": "tokens/s", "cores": cores, "kind": "port",
-                                    "sample": sample + f"; tokens/s = {T} / (128 x that)"}
+                                    "cpu_model": cpu_model(),
+                                    "sample": sample + f"; tokens/s = {T} / (128 x that); the --impl reference "
+                                                       "arm times full 128-apply steps"}
+            line["decision_path"] = decision_path_record()
         print(json.dumps(line), flush=True)
     pool.close()
 
@@ -706,6 +781,9 @@ def main():
     ap.add_argument("--config", choices=["c2", "c3", "c4", "c5"], default="c2",
                     help="c2 (default, the BASELINE metric's decode config) or c3 (prefill, tcgen05 path)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-max-steps", type=int, default=8,
+                    help="reference arm: full CPU steps timed (each ~2 s on 16 cores)")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (tcgen05 prefill) sub-record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

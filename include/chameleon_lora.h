@@ -112,6 +112,13 @@ CHAM_API int cham_pool_copy_out(const cham_pool* pool, size_t offset, size_t byt
 CHAM_API int cham_pool_set_prefill_route(cham_pool* pool, int min_tokens, int min_segment_tokens,
                                          int max_segment_tokens);
 
+/* Device-side error word of the pool's kernels (0 = none).  Kernels that meet a
+ * compiled-in limit only known on the device (segment count read from n_seg_dev, more than
+ * kPrefillMaxTiles prefill tiles, plan totals above max_tokens) leave y untouched and set
+ * it to CHAM_ERR_LIMIT.  Synchronises `stream`; clear != 0 resets the word.
+ * Pools are limited to 65535 pages and 65535 max_tokens (cham_pool_create). */
+CHAM_API int cham_pool_device_error(cham_pool* pool, int* device_error, int clear, void* stream);
+
 /* Debug: record a per-item timeline of the decode kernel into `dev_buf`
  * (2 x [sm_count][items_per_cta][8] u64 — shrink kernel then expand kernel: producer issue
  * ns, kind<<32|bytes, consumer start ns, consumer end ns).  NULL disables.  Not for production use (adds global stores). */

@@ -326,9 +326,10 @@ class PagedAdapterCache(AdapterCache):
     """AdapterCache whose resident set lives in an AdapterPool (pages of 8 rank rows).
 
     Token accounting is the reference's (size_tokens = 4 * rank); a page holds 8 rank rows
-    = 32 tokens, so for ranks that are multiples of 8 page and token accounting coincide and
-    the page allocator can never contradict a token-level decision as long as the pool has
-    at least capacity_tokens // 32 pages (checked in set_capacity).
+    = 32 tokens.  The constructor requires every catalog adapter's size_tokens to equal its
+    page count x 32 (ranks that are multiples of 8 under the default byte model), and
+    set_capacity caps the capacity at pool.n_pages x 32, so the page allocator can never
+    contradict a token-level decision.
 
     host_store: adapter_id -> packed pinned host tensor (AdapterPool.pack_host); the
     reference's host-memory adapter repository.  fill_stream: side stream for miss fills.
@@ -338,14 +339,21 @@ class PagedAdapterCache(AdapterCache):
     TOKENS_PER_PAGE = 32
 
     def __init__(self, cfg: CacheConfig, catalog: dict[str, AdapterSpec], pool, host_store=None,
-                 fill_stream=None, compute_stream=None):
+                 fill_stream=None, compute_stream=None, event_factory=None):
+        """event_factory(stream) -> an event recorded on `stream` (default torch.cuda.Event)."""
         super().__init__(cfg, catalog)
         import torch
 
         self._torch = torch
+        self._record = event_factory or self._record_cuda
         self.pool = pool
         if len(catalog) > pool.n_slots:
             raise ValueError(f"pool has {pool.n_slots} slots for a catalog of {len(catalog)} adapters")
+        bad = [aid for aid, spec in catalog.items()
+               if spec.size_tokens != -(-spec.rank // 8) * self.TOKENS_PER_PAGE]
+        if bad:
+            raise ValueError(f"page and token accounting disagree for {len(bad)} adapters (e.g. {bad[0]}): "
+                             "size_tokens must equal ceil(rank/8) * 32 (ranks multiples of 8)")
         self.slot_ids = {aid: i for i, aid in enumerate(catalog)}
         self.host_store = host_store if host_store is not None else {}
         self.fill_stream = fill_stream or torch.cuda.Stream(device=pool.device)
@@ -353,9 +361,15 @@ class PagedAdapterCache(AdapterCache):
         self._free_pages = list(range(pool.n_pages))
         heapq.heapify(self._free_pages)
         self._page_release: dict[int, object] = {}
+        self._slot_release: dict[int, object] = {}
         self._fill_events: dict[str, object] = {}
         self.fill_bytes = 0
         self.fill_count = 0
+
+    def _record_cuda(self, stream):
+        ev = self._torch.cuda.Event()
+        ev.record(stream)
+        return ev
 
     # -- slots / pages -----------------------------------------------------------------------
     def slot_of(self, adapter_id: str) -> int:
@@ -368,41 +382,56 @@ class PagedAdapterCache(AdapterCache):
     def max_capacity_tokens(self) -> int:
         return self.pool.n_pages * self.TOKENS_PER_PAGE
 
+    def set_capacity(self, tokens: int, hints: set[str], now: TimePoint) -> list[str]:
+        """The reference's set_capacity (adapter_cache.py:250-263) with the target capped at
+        the pool's physical size (n_pages x 32 tokens)."""
+        return super().set_capacity(min(int(tokens), self.max_capacity_tokens), hints, now)
+
+    def begin_load(self, adapter_id: str, now: TimePoint) -> None:
+        """The reference's begin_load (adapter_cache.py:144-151); the page check runs before any
+        state changes, so a CacheFault for lack of pages leaves the cache untouched."""
+        e = self.entries[adapter_id]
+        if not (e.resident or e.loading):
+            n = -(-e.spec.rank // 8)
+            if len(self._free_pages) < n:
+                raise CacheFault(f"no free pool pages for {adapter_id} (need {n}, {len(self._free_pages)} free)")
+        super().begin_load(adapter_id, now)
+
     def _on_begin_load(self, entry: AdapterEntry) -> None:
-        torch = self._torch
         aid = entry.spec.adapter_id
         rank = entry.spec.rank
         n = -(-rank // 8)
-        if len(self._free_pages) < n:
-            raise CacheFault(f"no free pool pages for {aid} (need {n}, {len(self._free_pages)} free)")
         pages = sorted(heapq.heappop(self._free_pages) for _ in range(n))
         fs = self.fill_stream
+        slot = self.slot_ids[aid]
+        ev = self._slot_release.pop(slot, None)
+        if ev is not None:
+            fs.wait_event(ev)  # the slot's unbind (compute stream) lands before this rebind
         for p in pages:
             ev = self._page_release.pop(p, None)
             if ev is not None:
                 fs.wait_event(ev)  # a kernel launched before the eviction may still read p
-        slot = self.slot_ids[aid]
         self.pool.set_slot(slot, rank, pages, stream=fs)
         src = self.host_store.get(aid)
         if src is not None:
             self.pool.fill_async(slot, src, stream=fs)
             self.fill_bytes += src.numel()
             self.fill_count += 1
-        ev = torch.cuda.Event()
-        ev.record(fs)
-        self._fill_events[aid] = ev
+        self._fill_events[aid] = self._record(fs)
 
     def _on_drop(self, entry: AdapterEntry) -> None:
-        torch = self._torch
         aid = entry.spec.adapter_id
         slot = self.slot_ids[aid]
         pages = self.pool.slot_pages[slot]
-        ev = torch.cuda.Event()
-        ev.record(self.compute_stream)
+        # unbind first, then record: the event covers every kernel that read the pages AND the
+        # unbind itself, so a later rebind of this slot or reuse of these pages (fill stream,
+        # which waits on it) is ordered after both
+        self.pool.set_slot(slot, 0, [], stream=self.compute_stream)
+        ev = self._record(self.compute_stream)
+        self._slot_release[slot] = ev
         for p in pages:
             self._page_release[p] = ev
             heapq.heappush(self._free_pages, p)
-        self.pool.set_slot(slot, 0, [], stream=self.compute_stream)
         self._fill_events.pop(aid, None)
 
     def fill_event(self, adapter_id: str):

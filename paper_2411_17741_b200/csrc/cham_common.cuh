@@ -122,6 +122,16 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   return v;
 }
 
+// A relaxed read that observed a release, followed by this fence, is an acquire pattern
+// (PTX memory model): later reads happen after the writes the release published.  Lowers to
+// CCTL.IVALL only (no MEMBAR), so the producer lane does not wait for its outstanding copies.
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
+
+// Order this thread's view of generic-proxy global writes before its async-proxy (TMA) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

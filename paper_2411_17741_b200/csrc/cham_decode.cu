@@ -1353,18 +1353,30 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       // v stores, proxy fence; publisher warp: gpu fence, page bit).  The mask was peeked when
       // the unit was claimed and is refreshed only while a needed page is still in flight.
       const unsigned need = page_bits(pg0, npg);
-      if (lane == 0 && ((unsigned)rdy & need) != need) {
-        const int* c = p.tile_ctr + job * NTL + tile;
-        while ((((unsigned)(rdy = ld_acquire_gpu(c))) & need) != need) __nanosleep(20);
+      if (lane == 0) {
+        if (((unsigned)rdy & need) != need) {
+          const int* c = p.tile_ctr + job * NTL + tile;
+          while ((((unsigned)(rdy = ld_acquire_gpu(c))) & need) != need) __nanosleep(20);
+        } else {
+          fence_acquire_gpu();  // acquire pattern for the relaxed peek
+        }
+        fence_proxy_async_global();
       }
       __syncwarp();
     } else if (fused && k == 0) {
       // the tile's v rows are complete once all np shrink units of (job, tile) published
       // (writers: v stores, proxy fence; publisher warp: gpu fence, counter).  The counter
       // was peeked when the unit was claimed; only a tile still in flight then is polled.
-      if (lane == 0 && rdy < np) {
-        const int* c = p.tile_ctr + job * NTL + tile;
-        while (ld_acquire_gpu(c) < np) __nanosleep(20);
+      if (lane == 0) {
+        if (rdy < np) {
+          const int* c = p.tile_ctr + job * NTL + tile;
+          while (ld_acquire_gpu(c) < np) __nanosleep(20);
+        } else {
+          // the counter was peeked relaxed: this fence turns that read into an acquire
+          // (happens-after the publishers' releases) before the v rows are read
+          fence_acquire_gpu();
+        }
+        fence_proxy_async_global();  // generic-proxy v stores -> the bulk copy below
       }
       __syncwarp();
     }

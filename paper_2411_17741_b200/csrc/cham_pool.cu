@@ -115,6 +115,11 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     return fail(CHAM_ERR_INVALID, "cham_pool_create: non-positive geometry");
   if (dtype != CHAM_F32 && dtype != CHAM_BF16)
     return fail(CHAM_ERR_INVALID, "cham_pool_create: dtype must be CHAM_F32 or CHAM_BF16");
+  // the step plan stores page ids and token rows as 16-bit values
+  if (n_pages > kMaxPoolPages)
+    return fail(CHAM_ERR_LIMIT, "cham_pool_create: n_pages exceeds " + std::to_string(kMaxPoolPages));
+  if (max_tokens > kMaxPoolTokens)
+    return fail(CHAM_ERR_LIMIT, "cham_pool_create: max_tokens exceeds " + std::to_string(kMaxPoolTokens));
   const int es = dtype == CHAM_F32 ? 4 : 2;
   const int atom_e = kRowBytes / es;
   int hin_max = 0;
@@ -317,6 +322,19 @@ int cham_pool_fill_async(cham_pool* pool, int slot, const void* host_src, size_t
 
 int cham_pool_fill_from_device(cham_pool* pool, int slot, const void* dev_src, size_t bytes, void* stream) {
   return fill_common(pool, slot, dev_src, bytes, stream, cudaMemcpyDeviceToDevice);
+}
+
+int cham_pool_device_error(cham_pool* pool, int* device_error, int clear, void* stream) {
+  if (!pool || !device_error) return fail(CHAM_ERR_INVALID, "cham_pool_device_error: null argument");
+  int v = 0;
+  CHAM_CUDA(cudaMemcpyAsync(&v, pool->d_ctr + 2, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CHAM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (clear && v) {
+    CHAM_CUDA(cudaMemsetAsync(pool->d_ctr + 2, 0, sizeof(int), (cudaStream_t)stream));
+    CHAM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  }
+  *device_error = v;
+  return CHAM_OK;
 }
 
 int cham_debug_set_trace(cham_pool* pool, void* dev_buf, int items_per_cta) {

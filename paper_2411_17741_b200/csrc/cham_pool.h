@@ -55,6 +55,9 @@ constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles;  // one parity set: dispatc
 constexpr size_t kPrefillVImg = 32768;                // V image bytes per (job, tile)
 inline size_t prefill_ctr_ints() { return 2 * kPrefillCtrSet + kPrefillMaxTiles; }
 
+constexpr int kMaxPoolPages = 65535;   // plan page ids are uint16 (cham_decode.cu Plan::pages)
+constexpr int kMaxPoolTokens = 65535;  // plan token rows are uint16 (Plan::perm)
+
 constexpr int kSplitCap = 128;         // decode expand tiles split into page halves per apply
 constexpr int kSplitTG = 4;            // tokens per decode tile (decode::TG)
 constexpr int kSplitNcb = 2048;        // bytes of one B row per decode expand unit

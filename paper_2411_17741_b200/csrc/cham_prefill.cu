@@ -809,9 +809,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           if (nex >= 2) pf_wait(p, &sm.vempty[vb], ((nex >> 1) - 1) & 1, 5, nex, u_id);
           // every phase-1 unit of the tile has published its partial V image
           const int need = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
-          if (cur_flag < need)
+          if (cur_flag < need) {
             while (ld_acquire_gpu(p.tile_cnt + u.tile) < need) __nanosleep(32);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
+          } else {
+            fence_acquire_gpu();  // the relaxed peek saw the count: acquire pattern before the V read
+          }
+          fence_proxy_async_global();
           const uint32_t vbytes = u.ks * u.vstride;
           PF_CHECK(vbytes <= VBUF && vbytes > 0 && u.tile < tl.n_tiles && u.job < p.n_jobs, 6, vbytes, u.tile);
           mbar_arrive_expect_tx(&sm.vfull[vb], vbytes);

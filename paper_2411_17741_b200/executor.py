@@ -81,7 +81,10 @@ class LoraStepExecutor:
 
     def __init__(self, pool: AdapterPool, max_requests: int = 4096, max_tokens: Optional[int] = None,
                  proj_groups: Optional[Sequence[Sequence[int]]] = None, stream=None, prefill_min_tokens: int = 64,
-                 route_hints: bool = True):
+                 route_hints: bool = True, graph_requests: Optional[int] = None):
+        """graph_requests: pad every upload to this many requests (slot -1, 0 tokens — K4 drops
+        them, so the segment table is unchanged) so that one captured step graph, whose K4
+        launch bakes in the request count, replays any batch of up to that many requests."""
         self.pool = pool
         # tcgen05 routing: segments >= prefill_min_tokens (bf16 pools; 0 disables).  With
         # route_hints the host passes each step's segment-length bounds, so only the kernel
@@ -96,9 +99,20 @@ class LoraStepExecutor:
         self.max_tokens = int(max_tokens or pool.max_tokens)
         self.proj_groups = [list(g) for g in (proj_groups or [[p] for p in range(pool.n_proj)])]
         self.stream = stream
+        if graph_requests is not None and not 0 < int(graph_requests) <= self.max_requests:
+            raise ValueError(f"graph_requests must be in [1, {self.max_requests}]")
+        self.graph_requests = None if graph_requests is None else int(graph_requests)
         self.req_dev = torch.zeros(3, self.max_requests, dtype=torch.int32, device=dev)
-        self.req_host = torch.zeros(3, self.max_requests, dtype=torch.int32, pin_memory=True)
+        # two pinned staging buffers, each reused only after its previous H2D copy completed
+        self._req_host = [torch.zeros(3, self.max_requests, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self._req_done = [None, None]
+        self._req_i = 0
         self.n_req = 0
+        self.route_class = (self.decode_launched, self.prefill_launched)
+        self._graph = None
+        self._graph_class = None
+        self._graph_io = None
+        self.recaptures = 0
         self.table = SegmentTable(
             perm=torch.zeros(self.max_tokens, dtype=torch.int32, device=dev),
             seg_off=torch.zeros(self.max_requests + 1, dtype=torch.int32, device=dev),
@@ -119,19 +133,35 @@ class LoraStepExecutor:
         total = int(ntok.sum())
         if total > self.max_tokens:
             raise ValueError(f"{total} tokens > max_tokens {self.max_tokens}")
-        h = self.req_host.numpy()
+        m = n if self.graph_requests is None else self.graph_requests
+        if n > m:
+            raise ValueError(f"{n} requests > graph_requests {m}")
+        b = self._req_i
+        self._req_i ^= 1
+        if self._req_done[b] is not None:
+            self._req_done[b].synchronize()  # this staging buffer's previous copy has been consumed
+        host = self._req_host[b]
+        h = host.numpy()
         h[0, :n] = req_slot
         h[1, :n] = req_rank
         h[2, :n] = req_ntok
+        if m > n:  # padding requests: no adapter, no tokens
+            h[0, n:m] = -1
+            h[1, n:m] = 0
+            h[2, n:m] = 0
         s = stream or torch.cuda.current_stream(self.pool.device)
         with torch.cuda.stream(s):
-            self.req_dev[:, :n].copy_(self.req_host[:, :n], non_blocking=True)
-        self.n_req = n
+            self.req_dev[:, :m].copy_(host[:, :m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s)
+        self._req_done[b] = ev
+        self.n_req = m
         if self.route_hints:
             lo, hi = segment_token_bounds(req_slot, req_rank, req_ntok)
             self.pool.set_prefill_route(self.prefill_min_tokens, lo, hi)
             self.prefill_launched = self.prefill_min_tokens > 0 and hi >= self.prefill_min_tokens
             self.decode_launched = not self.prefill_launched or lo < self.prefill_min_tokens
+        self.route_class = (self.decode_launched, self.prefill_launched)
         return total
 
     # -- device side (capturable) ------------------------------------------------------------
@@ -164,3 +194,42 @@ class LoraStepExecutor:
         self.build(stream)
         for layer in range(self.pool.n_layers):
             self.apply_layer(layer, xs_per_layer[layer], ys_per_layer[layer], stream)
+
+    # -- CUDA-graph step (capture once, replay per step) ---------------------------------
+    def capture(self, xs_per_layer, ys_per_layer, stream) -> None:
+        """Capture `run` (K4 + plan + every apply) over these activation buffers as one CUDA
+        graph.  The kernel families launched (decode GEMV and/or tcgen05 prefill) follow the
+        routing class of the last upload; `replay` re-captures when a later batch needs a
+        family the graph does not contain, so a replay never skips segments."""
+        torch.cuda.synchronize(self.pool.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            self.run(xs_per_layer, ys_per_layer)
+        self._graph = g
+        self._graph_class = self.route_class
+        self._graph_io = (xs_per_layer, ys_per_layer, stream)
+
+    def replay(self) -> None:
+        """Replay the captured step on its stream for the batch of the last upload."""
+        if self._graph is None:
+            raise RuntimeError("capture() the step before replay()")
+        need_dec, need_pre = self.route_class
+        has_dec, has_pre = self._graph_class
+        if (need_dec and not has_dec) or (need_pre and not has_pre):
+            # the routing class widened (e.g. the first prefill after decode-only steps): the
+            # graph would skip a kernel family, so capture one that launches both
+            self.recaptures += 1
+            xs, ys, stream = self._graph_io
+            stream.synchronize()
+            self.decode_launched = self.decode_launched or has_dec
+            self.prefill_launched = self.prefill_launched or has_pre
+            if self.route_hints:
+                self.pool.set_prefill_route(self.prefill_min_tokens, 0 if self.decode_launched else
+                                            self.prefill_min_tokens, -1 if self.prefill_launched else 0)
+            self.route_class = (self.decode_launched, self.prefill_launched)
+            self.capture(xs, ys, stream)
+        self._graph.replay()
+
+    def check_device_error(self, stream=None) -> None:
+        """Raise if any kernel of the steps so far met a device-side limit (synchronises)."""
+        self.pool.check_device_error(stream=stream)

@@ -108,6 +108,20 @@ class AdapterPool:
         self.slot_rank[slot] = int(rank)
         self.slot_pages[slot] = pages
 
+    # -- device errors -----------------------------------------------------------------
+    def device_error(self, clear: bool = True, stream=None) -> int:
+        """The kernels' device-side error word (0 = none); synchronises the stream."""
+        v = ctypes.c_int()
+        call("cham_pool_device_error", self.handle, ctypes.byref(v), 1 if clear else 0, _stream_ptr(stream))
+        return int(v.value)
+
+    def check_device_error(self, stream=None) -> None:
+        """Raise ChamError if a kernel hit a device-side limit (its apply left y untouched)."""
+        v = self.device_error(clear=True, stream=stream)
+        if v:
+            raise _lib.ChamError(v, "device kernel", "a launch met a compiled-in limit on the device "
+                                 "(segments, prefill tiles or plan tokens) and skipped its work")
+
     # -- routing -----------------------------------------------------------------------
     def set_prefill_route(self, min_tokens: int = 64, min_segment_tokens: int = 0,
                           max_segment_tokens: int = -1) -> None:
