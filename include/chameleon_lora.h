@@ -112,6 +112,17 @@ CHAM_API int cham_pool_copy_out(const cham_pool* pool, size_t offset, size_t byt
 CHAM_API int cham_pool_set_prefill_route(cham_pool* pool, int min_tokens, int min_segment_tokens,
                                          int max_segment_tokens);
 
+/* Cross-apply weight prefetch (no reference counterpart: the reference simulates the step,
+ * engine.py:67-77).  cham_pool_set_next_apply names the (layer, projections) that the caller
+ * launches right after the NEXT apply on this pool, with the same segment table and plan;
+ * it is consumed (cleared) by that apply.  Its CTAs, once they run out of units, pull the
+ * first `bytes` (cham_pool_set_l2_prefetch, default 0 = off) of the hinted apply's A blocks,
+ * in the hinted apply's unit order, into L2 — HBM work that does not depend on the current
+ * apply, done while its tail and the launch boundary leave bandwidth idle.  Results never
+ * depend on the hint (a wrong hint only wastes bandwidth).  n_projs <= 0 clears it. */
+CHAM_API int cham_pool_set_next_apply(cham_pool* pool, int layer, int n_projs, const int* projs);
+CHAM_API int cham_pool_set_l2_prefetch(cham_pool* pool, long long bytes);
+
 /* Device-side error word of the pool's kernels (0 = none).  Kernels that meet a
  * compiled-in limit only known on the device (segment count read from n_seg_dev, more than
  * kPrefillMaxTiles prefill tiles, plan totals above max_tokens) leave y untouched and set

@@ -55,6 +55,8 @@ SIGNATURES = {
     "cham_pool_fill_from_device": (c_int, [_P, c_int, _P, c_size_t, _P]),
     "cham_pool_set_prefill_route": (c_int, [_P, c_int, c_int, c_int]),
     "cham_pool_device_error": (c_int, [_P, _IP, c_int, _P]),
+    "cham_pool_set_next_apply": (c_int, [_P, c_int, c_int, _IP]),
+    "cham_pool_set_l2_prefetch": (c_int, [_P, ctypes.c_longlong]),
     "cham_debug_set_trace": (c_int, [_P, _P, c_int]),
     "cham_pool_copy_out": (c_int, [_P, c_size_t, c_size_t, _P, _P]),
     "cham_pack_adapter_host": (c_int, [_P, c_int, _P, _P, _P]),

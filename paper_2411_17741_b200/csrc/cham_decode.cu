@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include "cham_pool.h"
 
 namespace cham {
@@ -156,6 +158,12 @@ struct Params {
   const void* plan;           // Plan header + unit descriptors (cham_build_plan)
   long long desc_cap;
   int prefill_thr;            // segments routed to the tcgen05 kernels (cham_prefill.cu) are skipped
+  // next-apply L2 prefetch (cham_pool_set_next_apply): A blocks of the hinted apply's first
+  // nx_items shrink units (its unit order: job-major, descriptor order), claimed through ctr[5]
+  int nx_jobs;
+  int nx_items;
+  int nx_a_bytes;
+  long long nx_a_off[kMaxJobs];
 };
 
 // Per-stage record written by the producer, read by the consumers after the full barrier.
@@ -1485,6 +1493,32 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
   return seq;
 }
 
+// Out of units: pull the hinted next apply's first A blocks into L2 (evict_last, so they
+// survive until that apply's evict_first reads).  Items are the next apply's shrink units in
+// its own claim order (job-major, descriptor order over the SAME plan), 32 per claim of the
+// shared counter ctr[5], so the CTAs that finish first prefetch the most.
+__device__ __noinline__ void prefetch_next_apply(const Params& p, const Plan& pl, int lane) {
+  const int per_job = pl.totals[0];
+  const int total = min(p.nx_items, per_job * p.nx_jobs);
+  const UnitDesc* desc = reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan));
+  const uint64_t pol = policy_evict_last();
+  for (;;) {
+    int b = 0;
+    if (lane == 0) b = atomicAdd(p.ctr + 5, 32);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (b >= total) break;
+    const int u = b + lane;
+    if (u < total) {
+      const int job = u / per_job, di = u - job * per_job;
+      const int page = __ldg(&desc[di].aux);
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(
+                       p.base + (long long)page * p.page_bytes + p.nx_a_off[job]),
+                   "r"(p.nx_a_bytes), "l"(pol)
+                   : "memory");
+    }
+  }
+}
+
 // Marker stage (end of the unit stream).
 __device__ __forceinline__ void post_marker(Shared& sm, int seq, int kind) {
   const int st = seq % NSTAGE;
@@ -1535,6 +1569,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     seq = produce_all<T>(p, sm, seq, waited, mode);
     if (!waited) pdl_wait();
     if (lane == 0) post_marker(sm, seq, KIND_END);
+    if (p.nx_items > 0) prefetch_next_apply(p, sm.plan, lane);
   } else {
     const int ct = tid;  // consumer warps 0 .. GROUP_WARPS-1
     const int gw = ct >> 5;
@@ -1610,6 +1645,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     if (tid == 0) {
       p.ctr[0] = 0;
       p.ctr[4] = 0;
+      p.ctr[5] = 0;
       p.ctr[1] = 0;
     }
     __threadfence();
@@ -1776,6 +1812,13 @@ int decode_entry(cham_pool* pool, int layer, int n_jobs, const int* projs, const
   }
   prm.plan = plan;
   prm.prefill_thr = prefill_route_thr(pool);
+  if (pool->next_n > 0 && pool->l2_prefetch_bytes > 0 && mode == MODE_FUSED) {
+    prm.nx_jobs = pool->next_n;
+    prm.nx_a_bytes = pool->next_a_bytes;
+    prm.nx_items = (int)std::min<long long>(pool->l2_prefetch_bytes / pool->next_a_bytes, 1 << 30);
+    for (int j = 0; j < pool->next_n; ++j) prm.nx_a_off[j] = (long long)pool->next_a_off[j];
+  }
+  pool->next_n = 0;  // one-shot
   const bool pre = prm.prefill_thr < (1 << 30) && n_tokens >= prm.prefill_thr;
   if (pre && mode != MODE_FUSED && n_jobs > 1) {
     // the prefill kernel's TP halves take one projection: one call per job on its v columns

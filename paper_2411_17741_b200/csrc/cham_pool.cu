@@ -250,6 +250,31 @@ int cham_pool_set_prefill_route(cham_pool* pool, int min_tokens, int min_segment
   return CHAM_OK;
 }
 
+int cham_pool_set_next_apply(cham_pool* pool, int layer, int n_projs, const int* projs) {
+  if (!pool) return fail(CHAM_ERR_INVALID, "cham_pool_set_next_apply: null pool");
+  if (n_projs <= 0) {
+    pool->next_n = 0;
+    return CHAM_OK;
+  }
+  if (n_projs > cham::kMaxJobs || !projs) return fail(CHAM_ERR_INVALID, "cham_pool_set_next_apply: 1..max_jobs projections");
+  if (layer < 0 || layer >= pool->n_layers) return fail(CHAM_ERR_INVALID, "cham_pool_set_next_apply: layer out of range");
+  for (int j = 0; j < n_projs; ++j) {
+    if (projs[j] < 0 || projs[j] >= pool->n_proj) return fail(CHAM_ERR_INVALID, "cham_pool_set_next_apply: proj out of range");
+    if (pool->h_in[projs[j]] != pool->h_in[projs[0]])
+      return fail(CHAM_ERR_INVALID, "cham_pool_set_next_apply: projections must share h_in");
+    pool->next_a_off[j] = pool->a_off[(size_t)layer * pool->n_proj + projs[j]];
+  }
+  pool->next_a_bytes = kRowsPerPage * pool->h_in[projs[0]] * pool->es;
+  pool->next_n = n_projs;
+  return CHAM_OK;
+}
+
+int cham_pool_set_l2_prefetch(cham_pool* pool, long long bytes) {
+  if (!pool || bytes < 0) return fail(CHAM_ERR_INVALID, "cham_pool_set_l2_prefetch: null pool or negative budget");
+  pool->l2_prefetch_bytes = bytes;
+  return CHAM_OK;
+}
+
 int cham_pool_page_bytes(const cham_pool* pool, size_t* out) {
   if (!pool || !out) return fail(CHAM_ERR_INVALID, "null");
   *out = pool->page_bytes;

@@ -44,6 +44,13 @@ struct cham_pool {
   float* d_split = nullptr;            // decode page-half partials [kMaxJobs][kSplitCap][split_ncc][4][2048 B cols]
   int* d_split_ctr = nullptr;          // 2 parity x [kMaxJobs][kSplitCap][split_ncc]
   int split_ncc = 1;                   // 2048-byte column chunks of the widest h_out
+  // Next-apply hint (cham_pool_set_next_apply): the (layer, projections) the caller launches
+  // right after the next apply on the same plan.  That apply's CTAs, once out of units, pull
+  // the first l2_prefetch_bytes of the hinted apply's A blocks into L2 (one-shot).
+  int next_n = 0;
+  size_t next_a_off[cham::kMaxJobs] = {};
+  int next_a_bytes = 0;                // bytes of one page's A block of the hinted projections
+  long long l2_prefetch_bytes = 0;     // budget per hinted apply (0 = off)
 };
 
 namespace cham {

@@ -197,6 +197,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// the same without an L2 cache hint
+__device__ __forceinline__ void tma_load_2d_nohint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 // 2-D TMA tensor store smem -> global (bulk async-group of the issuing thread)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -236,6 +244,21 @@ __device__ __forceinline__ void crumb(const Params& p, int field, unsigned long 
 #endif
 #ifndef CHAM_PF_LATE_ALLOC
 #define CHAM_PF_LATE_ALLOC 0  // 1: tcgen05.alloc after griddepcontrol.wait (fault-hunt experiment)
+#endif
+#ifndef CHAM_PF_XPOL_NORMAL
+#define CHAM_PF_XPOL_NORMAL 1  // x load L2 policy: 0 evict_last, 1 evict_normal (default), 2 evict_first, 3 no hint.
+// evict_last faulted the context ("unspecified launch failure") in nearly every run when
+// another kernel had just rewritten x (dirty L2 lines) and the launches were PDL-chained;
+// 0 faults in 30 runs with any of 1-3 (scripts/fault_repro.py kb/e2e)
+#endif
+#ifndef CHAM_PF_NOPFMAP
+#define CHAM_PF_NOPFMAP 0  // fault-hunt experiment: 1 skips prefetch.tensormap
+#endif
+#ifndef CHAM_PF_PROXYFENCE
+#define CHAM_PF_PROXYFENCE 0  // fault-hunt experiment: 1 adds fence.proxy.async.global after griddepcontrol.wait
+#endif
+#ifndef CHAM_PF_NOACQ
+#define CHAM_PF_NOACQ 0  // fault-hunt experiment: 1 drops the acquire fence after a satisfied peek
 #endif
 #ifndef CHAM_PF_DRAIN
 #define CHAM_PF_DRAIN 1  // drain the MMA warp's commit arrivals before the CTA exits
@@ -294,6 +317,11 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ void x_load(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar, uint64_t pol) {
+  if (CHAM_PF_XPOL_NORMAL == 3) tma_load_2d_nohint(dst, map, c0, c1, bar);
+  else tma_load_2d(dst, map, c0, c1, bar, pol);
+}
 
 // ------------------------------------------------------------------ tiles and units
 struct Tile {
@@ -674,7 +702,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       }
     fence_mbar_init();
   }
-  if (warp == W_LOAD && lane < p.n_jobs) {
+  if (!CHAM_PF_NOPFMAP && warp == W_LOAD && lane < p.n_jobs) {
     prefetch_map(&p.maps[lane].x64);
     prefetch_map(&p.maps[lane].x1);
     prefetch_map(&p.maps[lane].y64);
@@ -693,6 +721,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   const uint32_t tmem = sm.tmem_base;
   crumb(p, 1, gtimer());
   pdl_wait();  // x, y, v and the workspaces may belong to the previous kernel
+  if (CHAM_PF_PROXYFENCE) fence_proxy_async_global();
   crumb(p, 2, gtimer());
   pdl_launch_dependents();
   if (!sm.flag) {
@@ -700,10 +729,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   } else if (warp == W_LOAD) {
     // ---------------------------------------------------------------- loader + dispatch
     const uint64_t pol_w = policy_evict_first();  // adapter pages: streamed
-#ifndef CHAM_PF_XPOL_NORMAL
-#define CHAM_PF_XPOL_NORMAL 0
-#endif
-    const uint64_t pol_x = CHAM_PF_XPOL_NORMAL ? policy_evict_normal() : policy_evict_last();  // x: re-read by the other job groups / K ranges
+    const uint64_t pol_x = CHAM_PF_XPOL_NORMAL == 1 ? policy_evict_normal() : CHAM_PF_XPOL_NORMAL == 2 ? policy_evict_first() : policy_evict_last();  // x: re-read by the other job groups / K ranges
     const uint64_t pol_y = policy_evict_first();
     int next = blockIdx.x;  // first unit static, the rest from the counter (one claim ahead)
     int claim = 0;
@@ -783,12 +809,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
               if (h * 64 >= u.m) continue;
               if (c64[h]) {
                 if (lane == 0)
-                  tma_load_2d(xdst + h * 64 * 128, &p.maps[u.job0].x64, kc * 64, rows[2 * h], &sm.full[st], pol_x);
+                  x_load(xdst + h * 64 * 128, &p.maps[u.job0].x64, kc * 64, rows[2 * h], &sm.full[st], pol_x);
               } else {
 #pragma unroll
                 for (int b = 2 * h; b < 2 * h + 2; ++b)
                   if (b * 32 + lane < u.m)
-                    tma_load_2d(xdst + (b * 32 + lane) * 128, &p.maps[u.job0].x1, kc * 64, rows[b], &sm.full[st], pol_x);
+                    x_load(xdst + (b * 32 + lane) * 128, &p.maps[u.job0].x1, kc * 64, rows[b], &sm.full[st], pol_x);
               }
             }
           }
@@ -811,7 +837,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int need = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
           if (cur_flag < need) {
             while (ld_acquire_gpu(p.tile_cnt + u.tile) < need) __nanosleep(32);
-          } else {
+          } else if (!CHAM_PF_NOACQ) {
             fence_acquire_gpu();  // the relaxed peek saw the count: acquire pattern before the V read
           }
           fence_proxy_async_global();

@@ -10,6 +10,7 @@ count never leaves the device), so a step replays as one graph.
 """
 from __future__ import annotations
 
+import os
 from typing import Callable, Optional, Sequence
 
 import numpy as np
@@ -18,6 +19,9 @@ import torch
 from . import _lib
 from .ops import SegmentTable, build_plan, build_segments, lora_apply_multi, lora_apply_table
 from .pool import AdapterPool
+
+
+DEFAULT_L2_PREFETCH_MB = 0
 
 
 def batch_arrays(batch, slot_of: Callable[[str], int], rank_of: Callable[[str], int]):
@@ -81,11 +85,19 @@ class LoraStepExecutor:
 
     def __init__(self, pool: AdapterPool, max_requests: int = 4096, max_tokens: Optional[int] = None,
                  proj_groups: Optional[Sequence[Sequence[int]]] = None, stream=None, prefill_min_tokens: int = 64,
-                 route_hints: bool = True, graph_requests: Optional[int] = None):
+                 route_hints: bool = True, graph_requests: Optional[int] = None,
+                 l2_prefetch_bytes: Optional[int] = None):
         """graph_requests: pad every upload to this many requests (slot -1, 0 tokens — K4 drops
         them, so the segment table is unchanged) so that one captured step graph, whose K4
         launch bakes in the request count, replays any batch of up to that many requests."""
         self.pool = pool
+        # cross-apply prefetch: each apply pulls the first l2_prefetch_bytes of the NEXT
+        # (layer, group) apply's A blocks into L2 once it runs out of units (its tail and the
+        # launch boundary leave HBM idle).  Env CHAM_L2_PREFETCH_MB overrides the default.
+        if l2_prefetch_bytes is None:
+            l2_prefetch_bytes = int(float(os.environ.get("CHAM_L2_PREFETCH_MB", DEFAULT_L2_PREFETCH_MB)) * (1 << 20))
+        self.l2_prefetch_bytes = int(l2_prefetch_bytes)
+        pool.set_l2_prefetch(self.l2_prefetch_bytes)
         # tcgen05 routing: segments >= prefill_min_tokens (bf16 pools; 0 disables).  With
         # route_hints the host passes each step's segment-length bounds, so only the kernel
         # family with work is launched (set before the step's plan is built / captured).
@@ -173,9 +185,20 @@ class LoraStepExecutor:
         build_plan(self.table, pool=self.pool, stream=stream)
         return self.table
 
-    def apply_layer(self, layer: int, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], stream=None):
-        """xs[g]: input of projection group g; ys[p]: output of projection p (in place)."""
+    def apply_layer(self, layer: int, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], stream=None,
+                    last: bool = True):
+        """xs[g]: input of projection group g; ys[p]: output of projection p (in place).
+        With last=False the step continues with layer + 1 (same plan): the final group's apply
+        prefetches that layer's first group."""
+        G = len(self.proj_groups)
         for g, projs in enumerate(self.proj_groups):
+            if self.l2_prefetch_bytes > 0:
+                if g + 1 < G:
+                    self.pool.set_next_apply(layer, self.proj_groups[g + 1])
+                elif not last and layer + 1 < self.pool.n_layers:
+                    self.pool.set_next_apply(layer + 1, self.proj_groups[0])
+                else:
+                    self.pool.set_next_apply()
             if len(projs) == 1:
                 lora_apply_table(xs[g], ys[projs[0]], self.table, pool=self.pool, layer=layer, proj=projs[0],
                                  stream=stream)
@@ -192,8 +215,9 @@ class LoraStepExecutor:
     def run(self, xs_per_layer, ys_per_layer, stream=None) -> None:
         """K4 + every (layer, group) apply, on `stream`."""
         self.build(stream)
-        for layer in range(self.pool.n_layers):
-            self.apply_layer(layer, xs_per_layer[layer], ys_per_layer[layer], stream)
+        L = self.pool.n_layers
+        for layer in range(L):
+            self.apply_layer(layer, xs_per_layer[layer], ys_per_layer[layer], stream, last=layer + 1 == L)
 
     # -- CUDA-graph step (capture once, replay per step) ---------------------------------
     def capture(self, xs_per_layer, ys_per_layer, stream) -> None:
@@ -228,7 +252,8 @@ class LoraStepExecutor:
                                             self.prefill_min_tokens, -1 if self.prefill_launched else 0)
             self.route_class = (self.decode_launched, self.prefill_launched)
             self.capture(xs, ys, stream)
-        self._graph.replay()
+        with torch.cuda.stream(self._graph_io[2]):
+            self._graph.replay()
 
     def check_device_error(self, stream=None) -> None:
         """Raise if any kernel of the steps so far met a device-side limit (synchronises)."""

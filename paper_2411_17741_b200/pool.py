@@ -108,6 +108,17 @@ class AdapterPool:
         self.slot_rank[slot] = int(rank)
         self.slot_pages[slot] = pages
 
+    # -- cross-apply weight prefetch ----------------------------------------------------
+    def set_next_apply(self, layer: int = -1, projs=()) -> None:
+        """Hint: the apply launched after the next one is (layer, projs) on the same plan
+        (cham_pool_set_next_apply; consumed by the next apply).  Empty projs clears it."""
+        projs = [int(p) for p in projs]
+        call("cham_pool_set_next_apply", self.handle, int(layer), len(projs), _lib.int_array(projs) if projs else None)
+
+    def set_l2_prefetch(self, nbytes: int) -> None:
+        """Budget of hinted A-block bytes an apply pulls into L2 once out of units (0 = off)."""
+        call("cham_pool_set_l2_prefetch", self.handle, int(nbytes))
+
     # -- device errors -----------------------------------------------------------------
     def device_error(self, clear: bool = True, stream=None) -> int:
         """The kernels' device-side error word (0 = none); synchronises the stream."""

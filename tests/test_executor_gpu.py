@@ -352,7 +352,10 @@ def test_c3_full_4096_tokens_two_layers():
 def test_prefill_stress_chained_launches_do_not_fault():
     """Soak of the tcgen05 prefill kernel at the C3 shape: 3 rounds x 1,200 PDL-chained
     launches (2 layers x (q/k/v + o) per step, 300 graph replays), each round ending with a
-    synchronisation and a device-error check; then one more step is checked against the oracle."""
+    synchronisation and a device-error check; then one more step is checked against the oracle.
+    Before every replay a copy kernel on the same stream rewrites the first layer's x (same
+    values): the serving pattern that made x loads with an L2 evict_last hint fault the
+    context in nearly every run."""
     from paper_2411_17741_b200.workload import prefill_batch, rank_of_id
 
     pids, pntok = prefill_batch(0)
@@ -367,8 +370,11 @@ def test_prefill_stress_chained_launches_do_not_fault():
             m.ex.run(m.xs, m.ys)
         s.synchronize()
         m.ex.capture(m.xs, m.ys, s)
+        x_src = m.xs[0][0].clone()
         for _ in range(3):
             for _ in range(300):
+                with torch.cuda.stream(s):
+                    m.xs[0][0].copy_(x_src)
                 m.ex.replay()
             s.synchronize()
             m.ex.check_device_error()
