@@ -107,7 +107,16 @@ constexpr int PQ = 16;             // publisher ring depth (tile counters to rel
 constexpr int GROUP_WARPS = 8;
 constexpr int GROUP_THREADS = GROUP_WARPS * 32;
 constexpr int NTHREADS = 32 + GROUP_THREADS;      // plan kernel; apply kernel adds the publisher warp
-constexpr int APPLY_THREADS = NTHREADS + 32;
+// Producer warps of the apply kernel.  With 2, producer pid issues the ring stages with
+// seq % 2 == pid (both walk the same unit stream: producer 0 claims the units and hands the
+// ids to producer 1 through a shared-memory queue), so two stages' issue latencies overlap.
+#ifndef CHAM_NPROD
+#define CHAM_NPROD 2
+#endif
+constexpr int NPROD = CHAM_NPROD;
+static_assert(NPROD == 1 || NPROD == 2, "one or two producer warps");
+constexpr int APPLY_THREADS = NTHREADS + 32 * NPROD;  // consumers, producer 0, publisher, producer 1
+constexpr int UQN = 8;  // unit-id queue depth, producer 0 -> producer 1
 static_assert(GROUP_THREADS == 2 * (tier_ncb(0) / 16) && GROUP_THREADS == 4 * (tier_ncb(1) / 16) &&
                   GROUP_THREADS == 8 * (tier_ncb(2) / 16),
               "K2 maps 2 << tier threads per 16-byte column chunk");
@@ -253,6 +262,7 @@ constexpr bool kStagger = CHAM_STAGGER != 0;
 #define CHAM_DEFER 0  // 1: set aside one not-yet-ready expand unit instead of waiting on it
 #endif
 constexpr bool kDefer = CHAM_DEFER != 0;
+static_assert(!(kDefer && CHAM_NPROD > 1), "the deferred-unit order is a per-producer decision (racy peeks)");
 #ifndef CHAM_STAGGER_1JOB
 #define CHAM_STAGGER_1JOB 0  // stagger gap for single-projection launches only
 #endif
@@ -278,6 +288,8 @@ struct Shared {
   unsigned pub_bits[PQ];
   uint64_t pub_full[PQ], pub_empty[PQ];
   int unit_mailbox;
+  int uq_id[UQN];  // unit ids, producer 0 -> producer 1
+  uint64_t uq_full[UQN], uq_empty[UQN];
   Schedule sched;
   Plan plan;
 };
@@ -545,6 +557,10 @@ __device__ __forceinline__ bool prologue(const Params& p, Shared& sm) {
       mbar_init(&sm.empty[i], GROUP_THREADS);
     }
     mbar_init(&sm.plan_bar, 1);
+    for (int i = 0; i < UQN; ++i) {
+      mbar_init(&sm.uq_full[i], 1);
+      mbar_init(&sm.uq_empty[i], 1);
+    }
     for (int i = 0; i < PQ; ++i) {
       mbar_init(&sm.pub_full[i], 1);
       mbar_init(&sm.pub_empty[i], 1);
@@ -1192,7 +1208,7 @@ __device__ __forceinline__ void pend_flush(PendingX& q, bool& waited, uint64_t p
 
 template <typename T>
 __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq, bool& waited, PendingX& pend, int job,
-                                            int4 da, int4 db) {
+                                            int4 da, int4 db, int pid) {
   constexpr int ES = Elem<T>::kBytes;
   const int lane = threadIdx.x & 31;
   const int nkc = n_kchunks<T>(p);
@@ -1205,6 +1221,7 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
   const Job& jb = p.jobs[job];
   const char* a_src = p.base + (long long)da.w * p.page_bytes + jb.a_off;
   for (int kc = 0; kc < nkc; ++kc, ++seq) {
+    if (NPROD > 1 && (seq & 1) != pid) continue;  // the other producer's stage
     const unsigned long long t_it = p.trace ? gtimer() : 0;
     const int stage = seq % NSTAGE;
     const int a0 = kc * (A_CHUNK / kAtomBytes);
@@ -1249,7 +1266,7 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
 template <typename T>
 __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq, bool& waited, PendingX& pend,
                                             bool fused, int job, int cc, int tile, int half, int tier, int4 da,
-                                            int4 db, int rdy, int unit) {
+                                            int4 db, int rdy, int unit, int pid) {
   constexpr int ES = Elem<T>::kBytes;
   pend_flush(pend, waited, policy_evict_last());
   const Plan& pl = sm.plan;
@@ -1282,7 +1299,9 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
   const int xm = half + 1;
   const int sidx = half >= 0 ? (job * kSplitCap + tile) * p.split_ncc + cc : 0;
   const Job& jb = p.jobs[job];
+  bool v_checked = false;  // this producer has seen the tile's v rows published
   for (int k = 0; k < nst; ++k, ++seq) {
+    if (NPROD > 1 && (seq & 1) != pid) continue;  // the other producer's stage
     const unsigned long long t_it = p.trace ? gtimer() : 0;
     const int stage = seq % NSTAGE;
     unsigned char* st = sm.stage[stage];
@@ -1371,7 +1390,9 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
         fence_proxy_async_global();
       }
       __syncwarp();
-    } else if (fused && k == 0) {
+    } else if (fused && !v_checked) {
+      // (first stage of the unit THIS producer issues: with two producers the other one
+      // issues every other stage and checks the counter itself)
       // the tile's v rows are complete once all np shrink units of (job, tile) published
       // (writers: v stores, proxy fence; publisher warp: gpu fence, counter).  The counter
       // was peeked when the unit was claimed; only a tile still in flight then is polled.
@@ -1387,6 +1408,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
         fence_proxy_async_global();  // generic-proxy v stores -> the bulk copy below
       }
       __syncwarp();
+      v_checked = true;
     }
     if (p.v_in) {
       // TP: v [position][v_stride] -> stage [page][token][8]: one 2-D box (8 ranks x TG
@@ -1415,20 +1437,46 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
 }
 
 template <typename T>
-__device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq, bool& waited, int mode) {
+__device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq, bool& waited, int mode, int pid) {
   PendingX pend;
   pend.n = 0;
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
   const bool fused = mode == MODE_FUSED;
   Schedule& sc = sm.sched;
-  if (lane == 0) build_schedule<T>(p, pl, mode, sc);
+  // producer 0 builds the schedule; producer 1 reads it only after receiving a unit id
+  // (the queue's mbarrier orders the schedule stores before)
+  if (pid == 0 && lane == 0) build_schedule<T>(p, pl, mode, sc);
   __syncwarp();
-  const int total = sc.start[sc.n];
+  const int total = pid == 0 ? sc.start[sc.n] : 0;
   const int NTL = pl.totals[1];
   const UnitDesc* desc = reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan));
   UnitQueue uq;
-  uq.init(p.ctr, total, CHAM_SH_DEPTH, lane, &sm.unit_mailbox);
+  if (pid == 0) uq.init(p.ctr, total, CHAM_SH_DEPTH, lane, &sm.unit_mailbox);
+  // the CTA's unit stream: producer 0 claims and forwards, producer 1 receives
+  int nq = 0;
+  auto next_unit = [&]() {
+    int u = -1;
+    if (NPROD == 1) return uq.next(lane);
+    const int q = nq % UQN;
+    if (pid == 0) {
+      u = uq.next(lane);
+      if (lane == 0) {
+        if (nq >= UQN) mbar_wait(&sm.uq_empty[q], ((nq / UQN) - 1) & 1);
+        sm.uq_id[q] = u;
+        mbar_arrive(&sm.uq_full[q]);
+      }
+    } else {
+      if (lane == 0) {
+        mbar_wait(&sm.uq_full[q], (nq / UQN) & 1);
+        u = sm.uq_id[q];
+        mbar_arrive(&sm.uq_empty[q]);
+      }
+      u = __shfl_sync(0xffffffffu, u, 0);
+    }
+    ++nq;
+    return u;
+  };
   // descriptor and (expand) tile-ready counter of a unit, fetched one unit ahead (relaxed)
   auto fetch = [&](int u, UnitPos& up, int4& a, int4& b, int& rdy) {
     up = locate<T>(p, pl, sc, u);
@@ -1439,7 +1487,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
       asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(rdy) : "l"(c) : "memory");
     }
   };
-  int unit = uq.next(lane);
+  int unit = next_unit();
   UnitPos up{};
   int4 da = make_int4(0, 0, 0, 0), db = da;
   int rdy = 0;
@@ -1462,17 +1510,17 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
   while (unit >= 0 || has_def) {
     if (has_def && (unit < 0 || __shfl_sync(0xffffffffu, tile_ready(def_rdy, np_of(def_a)), 0))) {
       seq = issue_expand<T>(p, sm, seq, waited, pend, fused, def_up.job, def_up.cc, def_up.di, def_up.half, def_up.tier, def_a,
-                            def_b, def_rdy, def_unit);
+                            def_b, def_rdy, def_unit, pid);
       has_def = false;
       if (unit < 0) break;
     }
-    const int nunit = uq.next(lane);
+    const int nunit = next_unit();
     UnitPos nup = up;
     int4 na = da, nb = db;
     int nrdy = 0;
     if (nunit >= 0) fetch(nunit, nup, na, nb, nrdy);
     if (up.kind == KIND_SHRINK) {
-      seq = issue_shrink<T>(p, sm, seq, waited, pend, up.job, da, db);
+      seq = issue_shrink<T>(p, sm, seq, waited, pend, up.job, da, db, pid);
     } else if (kDefer && fused && !has_def && !__shfl_sync(0xffffffffu, tile_ready(rdy, np_of(da)), 0)) {
       has_def = true;  // set aside; re-read below
       def_unit = unit;
@@ -1480,7 +1528,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
       def_a = da;
       def_b = db;
     } else {
-      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit);
+      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit, pid);
     }
     if (has_def) def_rdy = peek(def_up);
     unit = nunit;
@@ -1495,27 +1543,22 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
 
 // Out of units: pull the hinted next apply's first A blocks into L2 (evict_last, so they
 // survive until that apply's evict_first reads).  Items are the next apply's shrink units in
-// its own claim order (job-major, descriptor order over the SAME plan), 32 per claim of the
-// shared counter ctr[5], so the CTAs that finish first prefetch the most.
+// its own claim order (job-major, descriptor order over the SAME plan), spread statically
+// over the CTAs (item u -> CTA u % grid): one SM's TMA engine moves ~50 GB/s, so a CTA that
+// took many items would hold its SM's copy queue for tens of microseconds.
 __device__ __noinline__ void prefetch_next_apply(const Params& p, const Plan& pl, int lane) {
   const int per_job = pl.totals[0];
   const int total = min(p.nx_items, per_job * p.nx_jobs);
+  const int G = gridDim.x;
   const UnitDesc* desc = reinterpret_cast<const UnitDesc*>(static_cast<const char*>(p.plan) + sizeof(Plan));
   const uint64_t pol = policy_evict_last();
-  for (;;) {
-    int b = 0;
-    if (lane == 0) b = atomicAdd(p.ctr + 5, 32);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (b >= total) break;
-    const int u = b + lane;
-    if (u < total) {
-      const int job = u / per_job, di = u - job * per_job;
-      const int page = __ldg(&desc[di].aux);
-      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(
-                       p.base + (long long)page * p.page_bytes + p.nx_a_off[job]),
-                   "r"(p.nx_a_bytes), "l"(pol)
-                   : "memory");
-    }
+  for (int u = blockIdx.x + lane * G; u < total; u += 32 * G) {
+    const int job = u / per_job, di = u - job * per_job;
+    const int page = __ldg(&desc[di].aux);
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(
+                     p.base + (long long)page * p.page_bytes + p.nx_a_off[job]),
+                 "r"(p.nx_a_bytes), "l"(pol)
+                 : "memory");
   }
 }
 
@@ -1563,13 +1606,14 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
                                       // (acquired through pub_full)
       }
     }
-  } else if (warp == GROUP_WARPS) {
+  } else if (warp == GROUP_WARPS || warp == GROUP_WARPS + 2) {
+    const int pid = warp == GROUP_WARPS ? 0 : 1;
     bool waited = false;
     int seq = 0;
-    seq = produce_all<T>(p, sm, seq, waited, mode);
+    seq = produce_all<T>(p, sm, seq, waited, mode, pid);
     if (!waited) pdl_wait();
-    if (lane == 0) post_marker(sm, seq, KIND_END);
-    if (p.nx_items > 0) prefetch_next_apply(p, sm.plan, lane);
+    if (lane == 0 && (NPROD == 1 || (seq & 1) == pid)) post_marker(sm, seq, KIND_END);
+    if (pid == 0 && p.nx_items > 0) prefetch_next_apply(p, sm.plan, lane);
   } else {
     const int ct = tid;  // consumer warps 0 .. GROUP_WARPS-1
     const int gw = ct >> 5;
@@ -1645,7 +1689,6 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     if (tid == 0) {
       p.ctr[0] = 0;
       p.ctr[4] = 0;
-      p.ctr[5] = 0;
       p.ctr[1] = 0;
     }
     __threadfence();
