@@ -103,6 +103,19 @@ static_assert(CHAM_TIERS == 0 || (4 * tier_pitch(1) <= K2_B && 8 * tier_pitch(2)
 constexpr int K2_Y = K2_B;
 constexpr int K2_V = K2_Y + TG * NCB_SMALL;
 constexpr int K2_STAGE = K2_V + 8 * TG * kRowsPerPage * 4;  // v slice [page][token][8 rows]
+// Wide expand geometry for small-rank tiles (np <= CHAM_WIDE_NP pages): units of 2048 B per
+// B row (2048 bf16 columns), ONE page per stage, one consumer thread per 16-byte column chunk
+// holding all 8 rank rows — no sibling combine, no divergent y update, and twice the bytes
+// per unit of the tier-0 geometry, whose 1-page stages were consumer- and issue-bound
+// (0.9 us per 25 KB stage on C2).  Stage layout: B [8 rows][4096 B] | y [TG][4096 B] | v [TG][8].
+#ifndef CHAM_WIDE_NP
+#define CHAM_WIDE_NP 4
+#endif
+constexpr int kWideNp = CHAM_WIDE_NP;
+constexpr int TIER_W = 3;
+constexpr int NCB_WIDE = 4096;
+constexpr int K2W_Y = kRowsPerPage * NCB_WIDE;
+constexpr int K2W_V = K2W_Y + TG * NCB_WIDE;
 constexpr int PQ = 16;             // publisher ring depth (tile counters to release)
 constexpr int GROUP_WARPS = 8;
 constexpr int GROUP_THREADS = GROUP_WARPS * 32;
@@ -258,16 +271,12 @@ constexpr bool kStagger = CHAM_STAGGER != 0;
 #ifndef CHAM_ASPLIT
 #define CHAM_ASPLIT 1  // bulk copies per shrink stage's A chunk
 #endif
-#ifndef CHAM_DEFER
-#define CHAM_DEFER 0  // 1: set aside one not-yet-ready expand unit instead of waiting on it
-#endif
-constexpr bool kDefer = CHAM_DEFER != 0;
-static_assert(!(kDefer && CHAM_NPROD > 1), "the deferred-unit order is a per-producer decision (racy peeks)");
 #ifndef CHAM_STAGGER_1JOB
 #define CHAM_STAGGER_1JOB 0  // stagger gap for single-projection launches only
 #endif
 struct Schedule {
   int n;
+  int wide[MAX_BLOCKS];       // expand block in the wide geometry
   int start[MAX_BLOCKS + 1];  // unit prefix
   int kind[MAX_BLOCKS];       // KIND_SHRINK / KIND_EXPAND
   int a[MAX_BLOCKS], e[MAX_BLOCKS];  // LPT positions [a, e) of the class
@@ -275,6 +284,8 @@ struct Schedule {
 
 // rounded to 128 B: every stage base must satisfy the TMA tensor-copy alignment (TP v boxes)
 constexpr int STAGE_BYTES = ((K1_STAGE > K2_STAGE ? K1_STAGE : K2_STAGE) + 127) / 128 * 128;
+static_assert(kWideNp == 0 || K2W_V + TG * kRowsPerPage * 4 <= STAGE_BYTES, "wide expand stage layout");
+static_assert(GROUP_THREADS == NCB_WIDE / 16, "wide expand: one consumer thread per 16-byte column chunk");
 constexpr int SCRATCH_BYTES = TG * kMaxRank * 4;  // K2 v rows; K1 uses the first 1 KiB
 struct Shared {
   alignas(128) unsigned char stage[NSTAGE][STAGE_BYTES];
@@ -352,7 +363,7 @@ __device__ __forceinline__ int n_kchunks(const Params& p) {
 }
 template <typename T>
 __device__ __forceinline__ int n_colchunks(const Params& p, int tier) {
-  return ceil_div(p.h_out * Elem<T>::kBytes, tier_ncb(tier));
+  return ceil_div(p.h_out * Elem<T>::kBytes, tier == TIER_W ? NCB_WIDE : tier_ncb(tier));
 }
 
 // Builds the launch plan in shared memory (all NTHREADS threads).  It depends only on the
@@ -878,9 +889,9 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
     if (ct == 0) trace_consumer(p, seq, 2);
     const Meta& m = sm.meta[stage];
     const unsigned char* st = sm.stage[stage];
-    const float* Vst = reinterpret_cast<const float*>(st + K2_V);  // [page in stage][TG][8]
+    const float* Vst = reinterpret_cast<const float*>(st + (lpg == 0 ? K2W_V : K2_V));  // [page in stage][TG][8]
     if (active && !kNoCompute && m.npg > 0) {
-      if (lpg >= 2 || m.npg == 2) {
+      if (lpg != 1 || m.npg == 2) {
         // own page pg0 + h: all 8 rows, fully unrolled
         if (h < m.npg) {
           const unsigned char* Bg = st + h * m0.pitch;
@@ -956,7 +967,7 @@ __device__ __forceinline__ void expand_unit(const Params& p, Shared& sm, int& se
               continue;
             }
             float yv[EPV];
-            Elem<T>::unpack(lds128(st + K2_Y + t * m0.ncb + q * 16), yv);
+            Elem<T>::unpack(lds128(st + (lpg == 0 ? K2W_Y : K2_Y) + t * m0.ncb + q * 16), yv);
             if (m0.xm == 2) {  // combine stage: add half 0's partial
               const float4* pv = reinterpret_cast<const float4*>(st + (t * ncol_unit + q * EPV) * 4);
 #pragma unroll
@@ -1055,8 +1066,20 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
   const int J = p.n_jobs;
   const int ncc = n_colchunks<T>(p, 0);
   int n = 0, acc = 0;
-  auto add = [&](int kind, int a, int e) {
+  auto add = [&](int kind, int a, int e, bool wide = false) {
     const int t0 = pl.ex_start[a], t1 = pl.ex_start[e];
+    if (wide) {
+      const int units = J * n_colchunks<T>(p, TIER_W) * (t1 - t0);
+      if (units <= 0) return;
+      sc.kind[n] = kind;
+      sc.wide[n] = 1;
+      sc.a[n] = a;
+      sc.e[n] = e;
+      sc.start[n] = acc;
+      acc += units;
+      ++n;
+      return;
+    }
     const int nsp = max(0, min(pl.n_split, t1) - t0);  // split tiles inside the block
     const bool big_tier = kBigTier == 2;
     const int ncc2 = n_colchunks<T>(p, 2);
@@ -1066,6 +1089,7 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
                                           : J * ncc * (t1 - t0);
     if (units <= 0) return;
     sc.kind[n] = kind;
+    sc.wide[n] = 0;
     sc.a[n] = a;
     sc.e[n] = e;
     sc.start[n] = acc;
@@ -1084,7 +1108,16 @@ __device__ void build_schedule(const Params& p, const Plan& pl, int mode, Schedu
       for (int c = max(0, C - gap); c < C; ++c) add(KIND_EXPAND, pl.cls_pos[c], pl.cls_pos[c + 1]);
   } else {
     if (mode != MODE_EXPAND) add(KIND_SHRINK, pl.cls_pos[0], pl.cls_pos[C]);
-    if (mode != MODE_SHRINK) add(KIND_EXPAND, pl.cls_pos[0], pl.cls_pos[C]);
+    if (mode != MODE_SHRINK) {
+      // classes are in decreasing page count: the small-rank tail takes the wide geometry
+      int cw = C;
+      if (kWideNp > 0 && kSplitNp == 0 && kBigTier == 0) {
+        cw = 0;
+        while (cw < C && ceil_div(pl.seg_sr[pl.order[pl.cls_pos[cw]]] & 511, kRowsPerPage) > kWideNp) ++cw;
+      }
+      add(KIND_EXPAND, pl.cls_pos[0], pl.cls_pos[cw]);
+      if (cw < C) add(KIND_EXPAND, pl.cls_pos[cw], pl.cls_pos[C], true);
+    }
   }
   sc.start[n] = acc;
   sc.n = n;
@@ -1108,6 +1141,15 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
     r.cc = 0;
     r.half = -1;
     r.tier = 0;
+  } else if (sc.wide[b]) {
+    const int nccw = n_colchunks<T>(p, TIER_W);
+    const int per_tile = p.n_jobs * nccw;
+    r.tier = TIER_W;
+    r.half = -1;
+    r.di = pl.ex_start[sc.a[b]] + rel / per_tile;
+    const int jc = rel - (rel / per_tile) * per_tile;
+    r.job = jc / nccw;
+    r.cc = jc - r.job * nccw;
   } else {
     const int ncc = n_colchunks<T>(p, 0);
     const int per_tile = p.n_jobs * ncc;
@@ -1281,10 +1323,13 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
   const int slot = pl.seg_sr[s] >> 9;
   // tier 0: two consumer threads per 16-byte column chunk (EX_PAGES pages per stage; one page
   // is split in row halves); tier 2: eight threads, one page each, 8 pages per stage
-  const int lpg = tier == 2 ? 3 : 1;
-  const int pgs = tier == 2 ? 8 : EX_PAGES;
-  const int ncb = tier_ncb(tier);
-  const int pitch = tier_pitch(tier);
+  const bool wide = tier == TIER_W;
+  const int lpg = wide ? 0 : tier == 2 ? 3 : 1;
+  const int pgs = wide ? 1 : tier == 2 ? 8 : EX_PAGES;
+  const int ncb = wide ? NCB_WIDE : tier_ncb(tier);
+  const int pitch = wide ? K2W_Y : tier_pitch(tier);
+  const int yoff = wide ? K2W_Y : K2_Y;
+  const int voff = wide ? K2W_V : K2_V;
   const int ncol_unit = ncb / ES;
   const int col0 = cc * ncol_unit;
   const int ncols = min(ncol_unit, p.h_out - col0);
@@ -1325,7 +1370,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
         bulk_g2s(st, p.split_buf + (long long)sidx * TG * ncol_unit, part_bytes * tcount, &sm.full[stage], pol_w);
       }
       if (lane < tcount) {
-        bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
+        bulk_g2s(st + yoff + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
       }
       __syncwarp();
       continue;
@@ -1347,7 +1392,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
     if (p.v_in && npg_in < npg) {
       for (int c2 = lane; c2 < (npg - npg_in) * tcount; c2 += 32) {
         const int hh = npg_in + c2 / tcount, t = c2 % tcount;
-        float4* z = reinterpret_cast<float4*>(st + K2_V + (hh * TG + t) * kRowsPerPage * 4);
+        float4* z = reinterpret_cast<float4*>(st + voff + (hh * TG + t) * kRowsPerPage * 4);
         z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
         z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -1374,7 +1419,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       waited = true;
     }
     if (y_here && lane < tcount)
-      bulk_g2s(st + K2_Y + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
+      bulk_g2s(st + yoff + lane * ncb, jb.y + ((long long)row * p.h_out + col0) * ES, y_bytes, &sm.full[stage], pol_w);
     if (fused && kPageReady) {
       // this stage's v rows are final once the shrink units of ITS pages published (writers:
       // v stores, proxy fence; publisher warp: gpu fence, page bit).  The mask was peeked when
@@ -1416,12 +1461,12 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
       if (lane < npg_in)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
-            "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(st + K2_V + lane * TG * kRowsPerPage * 4)),
+            "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(st + voff + lane * TG * kRowsPerPage * 4)),
             "l"(reinterpret_cast<uint64_t>(&p.vmap)), "r"(job * p.v_cols + (pg0 + lane) * kRowsPerPage), "r"(pos0),
             "r"(smem_u32(&sm.full[stage])), "l"(pol_w)
             : "memory");
     } else if (lane == 0) {
-      bulk_g2s(st + K2_V, p.vws + job * p.vws_job_stride + vbase + pg0 * TG * kRowsPerPage, v_bytes, &sm.full[stage],
+      bulk_g2s(st + voff, p.vws + job * p.vws_job_stride + vbase + pg0 * TG * kRowsPerPage, v_bytes, &sm.full[stage],
                pol_w);
     }
     if (lane == 0) {
@@ -1487,55 +1532,33 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
       asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(rdy) : "l"(c) : "memory");
     }
   };
-  int unit = next_unit();
-  UnitPos up{};
-  int4 da = make_int4(0, 0, 0, 0), db = da;
-  int rdy = 0;
-  if (unit >= 0) fetch(unit, up, da, db, rdy);
-  // One expand unit whose tile was still in flight when its turn came may be set aside while
-  // the following units stream (its counter is re-read, relaxed, one unit ahead).
-  bool has_def = false;
-  int def_unit = 0, def_rdy = 0;
-  UnitPos def_up{};
-  int4 def_a = da, def_b = db;
-  auto peek = [&](const UnitPos& u) {
-    int v = 0;
-    if (lane == 0) {
-      const int* c = p.tile_ctr + u.job * NTL + u.di;
-      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-    }
-    return v;
+  // Units are fetched (descriptor loads from L2, tile-counter peek) two units ahead of the
+  // one being issued, so a stream of one-stage units does not wait on the L2 round trip.
+  struct Fetched {
+    int unit, rdy;
+    UnitPos up;
+    int4 a, b;
   };
-  auto np_of = [](const int4& a) { return (a.z >> 8) & 0xff; };
-  while (unit >= 0 || has_def) {
-    if (has_def && (unit < 0 || __shfl_sync(0xffffffffu, tile_ready(def_rdy, np_of(def_a)), 0))) {
-      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, def_up.job, def_up.cc, def_up.di, def_up.half, def_up.tier, def_a,
-                            def_b, def_rdy, def_unit, pid);
-      has_def = false;
-      if (unit < 0) break;
-    }
-    const int nunit = next_unit();
-    UnitPos nup = up;
-    int4 na = da, nb = db;
-    int nrdy = 0;
-    if (nunit >= 0) fetch(nunit, nup, na, nb, nrdy);
-    if (up.kind == KIND_SHRINK) {
-      seq = issue_shrink<T>(p, sm, seq, waited, pend, up.job, da, db, pid);
-    } else if (kDefer && fused && !has_def && !__shfl_sync(0xffffffffu, tile_ready(rdy, np_of(da)), 0)) {
-      has_def = true;  // set aside; re-read below
-      def_unit = unit;
-      def_up = up;
-      def_a = da;
-      def_b = db;
-    } else {
-      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, up.job, up.cc, up.di, up.half, up.tier, da, db, rdy, unit, pid);
-    }
-    if (has_def) def_rdy = peek(def_up);
-    unit = nunit;
-    up = nup;
-    da = na;
-    db = nb;
-    rdy = nrdy;
+  auto take = [&](Fetched& f) {
+    f.unit = next_unit();
+    f.rdy = 0;
+    if (f.unit >= 0) fetch(f.unit, f.up, f.a, f.b, f.rdy);
+  };
+  Fetched f0, f1;
+  take(f0);
+  f1.unit = -1;
+  if (f0.unit >= 0) take(f1);
+  while (f0.unit >= 0) {
+    Fetched f2;
+    f2.unit = -1;
+    if (f1.unit >= 0) take(f2);
+    if (f0.up.kind == KIND_SHRINK)
+      seq = issue_shrink<T>(p, sm, seq, waited, pend, f0.up.job, f0.a, f0.b, pid);
+    else
+      seq = issue_expand<T>(p, sm, seq, waited, pend, fused, f0.up.job, f0.up.cc, f0.up.di, f0.up.half, f0.up.tier, f0.a,
+                            f0.b, f0.rdy, f0.unit, pid);
+    f0 = f1;
+    f1 = f2;
   }
   pend_flush(pend, waited, policy_evict_last());
   return seq;
