@@ -49,6 +49,16 @@ WORKLOAD_C3 = ("C3: Llama-2-7B q/k/v/o LoRA (h=4096, 32 layers) prefill, 64 segm
                "64 adapters with power-law ranks (prefill_batch seed = rank), tcgen05 path")
 
 
+L2_NOTE = ("inputs larger than L2: each step streams every distinct adapter's pages for all 128 "
+           "(layer, proj) blocks (8 GB at C2) through the 126 MB L2")
+
+
+def c2_config(world: int, mode: str) -> dict:
+    """The C2 `config` object, printed identically by both arms (the driver's same_config)."""
+    return {"workload": WORKLOAD_C2, "global_batch": T_DECODE * world, "seq_len": 1,
+            "parallelism": f"replicas x{world}", "launch_mode": mode, "l2": L2_NOTE}
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -240,9 +250,7 @@ def run_reference(args, rank: int, world: int):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": n, "warmup": 1 if args.warmup > 0 else 0, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD_C2, "global_batch": T_DECODE * world, "seq_len": 1,
-                   "parallelism": f"replicas x{world}", "launch_mode": args.mode,
-                   "l2": "n/a (CPU)"},
+        "config": c2_config(world, args.mode),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "cpu_model": cpu_model(),
                          "sample": sample + f"; median of {n} timed full steps (--steps {args.steps} capped at "
@@ -254,7 +262,10 @@ def run_reference(args, rank: int, world: int):
 
 
 # --------------------------------------------------------------------------- GPU path
-def run_ours(args, rank: int, world: int):
+def measure(config: str, args, rank: int, world: int, e2e: bool = True) -> dict:
+    """Build the config's pool, batch and step graph on this rank's GPU and time it: K step
+    replays (CUDA events, max over ranks), the apply-only graph (roofline), and optionally the
+    host-buffer e2e loop.  Returns the raw measurements for the JSON line."""
     import torch
     import torch.distributed as dist
 
@@ -265,7 +276,7 @@ def run_ours(args, rank: int, world: int):
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
-    if args.config == "c3":
+    if config == "c3":
         # C3: 64 prefill segments x 64 tokens, one distinct adapter each (prefill_batch(seed=rank))
         pids, pntok = prefill_batch(rank)
         ids = list(dict.fromkeys(pids))
@@ -351,8 +362,9 @@ def run_ours(args, rank: int, world: int):
     barrier()
     torch.cuda.synchronize(dev)
     step_ms = ev0.elapsed_time(ev1) / args.steps
-    # apply-only graph for the roofline (the decode kernel launches alone)
-    reps = max(3, args.steps)
+    # apply-only graph for the roofline (the apply kernels launch alone), at least ~200 ms of
+    # replays so the clock sampler sees the load
+    reps = max(args.steps, int(200.0 / max(step_ms, 1e-3)) + 1)
     with torch.cuda.stream(s):
         ev0.record(s)
         for _ in range(reps):
@@ -361,7 +373,7 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize(dev)
     apply_ms = ev0.elapsed_time(ev1) / reps
     step_ms = max_over_ranks(step_ms)
-    apply_ms_max = max_over_ranks(apply_ms)
+    apply_ms = max_over_ranks(apply_ms)
 
     # ---- e2e: through the executor with host buffers (pinned H2D request table + hidden
     #      state, step graph, D2H of the last projection's output), wall clock over the steps
@@ -390,104 +402,138 @@ def run_ours(args, rank: int, world: int):
             x_stage[b].copy_(x_host, non_blocking=True)
             ev_x[b] = record(cs)
 
-    n_total = 0 if os.environ.get("BENCH_NO_E2E") else args.warmup + args.steps  # fault-hunt experiments only
-    stage_input(0)
-    t0 = time.perf_counter()
-    for i in range(n_total):
-        if i == args.warmup:
-            s.synchronize()
-            cs.synchronize()
-            barrier()
-            t0 = time.perf_counter()
-            stage_input(i & 1)  # this step's input transfer belongs to the timed region
-        b = i & 1
-        if i + 1 < n_total:
-            stage_input(b ^ 1)  # the next step's input streams in while this step computes
-        if ev_up is not None:
-            ev_up.synchronize()  # the pinned request staging was consumed by the previous upload
-        with torch.cuda.stream(s):
-            s.wait_event(ev_x[b])
-            xs[0][0].copy_(x_stage[b])
-            ev_xfree[b] = record(s)
-            ex.upload(req_slot, req_rank, req_ntok, stream=s)
-            ev_up = record(s)
-            if ev_yfree[b] is not None:
-                s.wait_event(ev_yfree[b])
-            g_step.replay()
-            y_stage[b].copy_(ys[N_LAYERS - 1][N_PROJ - 1])
-            ev_y[b] = record(s)
-        with torch.cuda.stream(cs):
-            cs.wait_event(ev_y[b])
-            y_host[b].copy_(y_stage[b], non_blocking=True)  # the step's result to the host
-            ev_yfree[b] = record(cs)
-    s.synchronize()
-    cs.synchronize()
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    n_total = args.warmup + args.steps if e2e and not os.environ.get("BENCH_NO_E2E") else 0
+    e2e_s = None
+    if n_total:
+        stage_input(0)
+        t0 = time.perf_counter()
+        for i in range(n_total):
+            if i == args.warmup:
+                s.synchronize()
+                cs.synchronize()
+                barrier()
+                t0 = time.perf_counter()
+                stage_input(i & 1)  # this step's input transfer belongs to the timed region
+            b = i & 1
+            if i + 1 < n_total:
+                stage_input(b ^ 1)  # the next step's input streams in while this step computes
+            if ev_up is not None:
+                ev_up.synchronize()  # the pinned request staging was consumed by the previous upload
+            with torch.cuda.stream(s):
+                s.wait_event(ev_x[b])
+                xs[0][0].copy_(x_stage[b])
+                ev_xfree[b] = record(s)
+                ex.upload(req_slot, req_rank, req_ntok, stream=s)
+                ev_up = record(s)
+                if ev_yfree[b] is not None:
+                    s.wait_event(ev_yfree[b])
+                g_step.replay()
+                y_stage[b].copy_(ys[N_LAYERS - 1][N_PROJ - 1])
+                ev_y[b] = record(s)
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_y[b])
+                y_host[b].copy_(y_stage[b], non_blocking=True)  # the step's result to the host
+                ev_yfree[b] = record(cs)
+        s.synchronize()
+        cs.synchronize()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
     clk.__exit__()
+    err = pool.device_error(clear=True, stream=s)  # 0: no kernel met a device-side limit
 
     # ---- algorithmic bytes / flops from the rank's segment table
     perm, off, sl, rk = ex.table.to_host()
     lp = N_LAYERS * N_PROJ
     bytes_step, adapter_bytes_step = step_bytes(off, sl, rk, T, H, 2, N_LAYERS, groups)
-    bytes_step, adapter_bytes_step = int(bytes_step), int(adapter_bytes_step)
     flops_step = int(2 * sum(int(rk[i]) * int(off[i + 1] - off[i]) for i in range(len(sl))) * (H + H) * lp)
-    hbm_peak, bf16_peak, peak_kind = peaks()
-    apply_launches = N_LAYERS * len(groups)
-    achieved = bytes_step / (apply_ms * 1e-3) / 1e9
-
-    if rank == 0:
-        tokens_total = T * world
-        value = tokens_total / (step_ms * 1e-3)
-        if args.config == "c3":
-            workload = WORKLOAD_C3
-            kernels = "prefill::fused_kernel (tcgen05, TMEM accumulators; shrink -> per-tile V images -> expand, PDL-chained) per apply"
-        else:
-            workload = WORKLOAD_C2
-            kernels = "decode::lora_apply_kernel<bf16> (shrink and expand units from one queue, per-tile v-ready counters, PDL-chained)"
-        line = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload,
-                       "global_batch": tokens_total, "seq_len": int(req_ntok.max()), "parallelism": f"replicas x{world}",
-                       "launch_mode": args.mode,
-                       "l2": "inputs larger than L2: each step streams 8 GB of distinct adapter pages "
-                             "(128 (layer,proj) blocks) through the 126 MB L2"},
-            "adapter_read_gbs": adapter_bytes_step / (step_ms * 1e-3) / 1e9,
-            "adapter_read_frac_of_peak": adapter_bytes_step / (step_ms * 1e-3) / 1e9 / hbm_peak,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "kernel": kernels,
-                         "bytes_per_step": bytes_step,
-                         "bytes_formula": "SURVEY 8(d) per (layer, proj): distinct adapters' A+B once, y read+write; "
-                                          "x once per launch group (q/k/v share one staged input)",
-                         "launches_per_step": apply_launches,
-                         "algorithmic_bytes_per_launch": bytes_step / apply_launches,
-                         "avg_launch_us": apply_ms * 1e3 / apply_launches,
-                         "traffic": traffic_per_launch(args.config),
-                         "traffic_source": "profiles/traffic_%s.json (ncu --set full, cold L2, DRAM read+write "
-                                           "bytes per launch, mean of one q/k/v and one o launch)" % args.config},
-            "flops_per_step": flops_step,
-            "tensor_frac_of_peak": flops_step / (apply_ms * 1e-3) / 1e12 / bf16_peak,
-            "e2e": {"value": tokens_total / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                    "mode": "every step: LoraStepExecutor.upload (pinned H2D of the request table), pinned H2D of "
-                            "the hidden state and pinned D2H of the output on a copy stream overlapping the "
-                            "neighbouring steps' kernels, step graph; wall clock over all steps"},
-            "gpu_launches": args.steps * ex.launches_per_step(),
-            "clocks": clk.summary(),
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            from bench_decisions import cpu_model
-
-            t_lp, cores, sample = cpu_oracle_sample(batch, seconds=args.cpu_seconds, ntok=list(req_ntok))
-            line["cpu_baseline"] = {"value": T / (t_lp * lp), "unit": "tokens/s", "cores": cores, "kind": "port",
-                                    "cpu_model": cpu_model(),
-                                    "sample": sample + f"; tokens/s = {T} / (128 x that); the --impl reference "
-                                                       "arm times full 128-apply steps"}
-            line["decision_path"] = decision_path_record()
-        print(json.dumps(line), flush=True)
+    out = {"T": T, "batch": batch, "req_ntok": req_ntok, "groups": groups, "step_ms": step_ms,
+           "apply_ms": apply_ms, "e2e_s": e2e_s, "h2d": h2d, "d2h": d2h, "bytes_step": int(bytes_step),
+           "adapter_bytes_step": int(adapter_bytes_step), "flops_step": flops_step,
+           "launches_per_step": ex.launches_per_step(), "apply_launches": N_LAYERS * len(groups),
+           "clocks": clk.summary(), "device_error": err}
     pool.close()
+    del xs, ys, ex, g_step, g_apply
+    torch.cuda.empty_cache()
+    return out
+
+
+def roofline_record(m: dict, config: str) -> dict:
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    achieved = m["bytes_step"] / (m["apply_ms"] * 1e-3) / 1e9
+    if config == "c3":
+        kernel = ("prefill::fused_kernel (tcgen05, TMEM accumulators; shrink -> per-tile V images -> expand, "
+                  "PDL-chained) per apply")
+    else:
+        kernel = ("decode::lora_apply_kernel<bf16> (shrink and expand units from one queue, per-tile v-ready "
+                  "counters, PDL-chained)")
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "peak_kind": peak_kind, "kernel": kernel,
+            "bytes_per_step": m["bytes_step"],
+            "bytes_formula": "SURVEY 8(d) per (layer, proj): distinct adapters' A+B once, y read+write; "
+                             "x once per launch group (q/k/v share one staged input)",
+            "launches_per_step": m["apply_launches"],
+            "algorithmic_bytes_per_launch": m["bytes_step"] / m["apply_launches"],
+            "avg_launch_us": m["apply_ms"] * 1e3 / m["apply_launches"],
+            "traffic": traffic_per_launch(config),
+            "traffic_source": "profiles/traffic_%s.json (ncu --set full, cold L2, DRAM read+write "
+                              "bytes per launch, mean of one q/k/v and one o launch)" % config}
+
+
+def run_ours(args, rank: int, world: int):
+    m = measure(args.config, args, rank, world, e2e=True)
+    c3 = None
+    if args.config == "c2" and not args.no_c3:
+        # the tcgen05 prefill path measured in the same driver run (C3 sub-record, no e2e loop)
+        c3 = measure("c3", args, rank, world, e2e=False)
+    if rank != 0:
+        return
+    hbm_peak, bf16_peak, _ = peaks()
+    T = m["T"]
+    tokens_total = T * world
+    value = tokens_total / (m["step_ms"] * 1e-3)
+    if args.config == "c3":
+        config = {"workload": WORKLOAD_C3, "global_batch": tokens_total, "seq_len": int(m["req_ntok"].max()),
+                  "parallelism": f"replicas x{world}", "launch_mode": args.mode,
+                  "l2": "inputs larger than L2: each step streams 16.8 GB of activations and adapter pages"}
+    else:
+        config = c2_config(world, args.mode)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["step_ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": config,
+        "adapter_read_gbs": m["adapter_bytes_step"] / (m["step_ms"] * 1e-3) / 1e9,
+        "adapter_read_frac_of_peak": m["adapter_bytes_step"] / (m["step_ms"] * 1e-3) / 1e9 / hbm_peak,
+        "roofline": roofline_record(m, args.config),
+        "flops_per_step": m["flops_step"],
+        "tensor_frac_of_peak": m["flops_step"] / (m["apply_ms"] * 1e-3) / 1e12 / bf16_peak,
+        "e2e": {"value": tokens_total / m["e2e_s"], "unit": "tokens/s", "h2d_bytes_per_step": m["h2d"],
+                "d2h_bytes_per_step": m["d2h"], "ms_per_step": m["e2e_s"] * 1e3,
+                "mode": "every step: LoraStepExecutor.upload (pinned H2D of the request table), pinned H2D of "
+                        "the hidden state and pinned D2H of the output on a copy stream overlapping the "
+                        "neighbouring steps' kernels, step graph; wall clock over all steps"},
+        "gpu_launches": args.steps * m["launches_per_step"],
+        "clocks": m["clocks"],
+        "device_error": m["device_error"],
+    }
+    if c3 is not None:
+        line["c3"] = {
+            "workload": WORKLOAD_C3, "tokens_s": c3["T"] * world / (c3["step_ms"] * 1e-3),
+            "ms_per_step": c3["step_ms"], "steps": args.steps, "warmup": args.warmup,
+            "roofline": roofline_record(c3, "c3"),
+            "tensor_frac_of_peak": c3["flops_step"] / (c3["apply_ms"] * 1e-3) / 1e12 / bf16_peak,
+            "clocks": c3["clocks"], "device_error": c3["device_error"],
+            "gpu_launches": args.steps * c3["launches_per_step"]}
+        line["gpu_launches"] += line["c3"]["gpu_launches"]
+    if world == 1 and not args.no_cpu_baseline:
+        from bench_decisions import cpu_model
+
+        lp = N_LAYERS * N_PROJ
+        t_lp, cores, sample = cpu_oracle_sample(m["batch"], seconds=args.cpu_seconds, ntok=list(m["req_ntok"]))
+        line["cpu_baseline"] = {"value": T / (t_lp * lp), "unit": "tokens/s", "cores": cores, "kind": "port",
+                                "cpu_model": cpu_model(),
+                                "sample": sample + f"; tokens/s = {T} / (128 x that); the --impl reference "
+                                                   "arm times full 128-apply steps"}
+        line["decision_path"] = decision_path_record()
+    print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------- C4: cache with misses
