@@ -79,6 +79,40 @@ _FIXED_WEIGHTS = {
 }
 
 
+def _jsonable(v):
+    if isinstance(v, (set, frozenset)):
+        return sorted(v)
+    if isinstance(v, (list, tuple)):
+        return list(v)
+    return v
+
+
+def _logged(name: str):
+    """Record the call in `self.op_log` (when not None) as {"op", "args", "ret"} or
+    {"op", "args", "raises"}: the replayable decision trace (serving.replay_ops, the format of
+    tests/golden/cache_traces.json).  Iterable arguments are materialised first."""
+    def deco(fn):
+        def wrapped(self, *args):
+            log = self.op_log
+            if log is None:
+                return fn(self, *args)
+            if name == "prefetch_candidates":
+                args = (list(args[0]),) + tuple(args[1:])
+            rec = {"op": name, "args": [_jsonable(a) for a in args]}
+            try:
+                ret = fn(self, *args)
+            except (InsufficientEvictableMemory, CacheFault) as ex:
+                rec["raises"] = type(ex).__name__
+                log.append(rec)
+                raise
+            rec["ret"] = [ret.hit, ret.load_bytes] if isinstance(ret, AcquireResult) else _jsonable(ret)
+            log.append(rec)
+            return ret
+        wrapped.__name__, wrapped.__doc__, wrapped.__wrapped__ = fn.__name__, fn.__doc__, fn
+        return wrapped
+    return deco
+
+
 def _pins(e: AdapterEntry) -> bool:
     """Counts toward non_evictable_tokens: in use by a running request, or in flight."""
     return (e.resident and e.rc > 0) or e.loading
@@ -101,6 +135,7 @@ class AdapterCache:
         self.loads = 0
         self._arrivals: dict[str, deque] = {}
         self._pinned_tokens = 0
+        self.op_log: Optional[list] = None  # set to [] to record the decision trace
         self._log2 = {aid: math.log2(spec.size_tokens) for aid, spec in catalog.items()}
 
     # -- residency and reference counting ------------------------------------------------
@@ -126,6 +161,7 @@ class AdapterCache:
         if after != before:
             self._pinned_tokens += e.size_tokens if after else -e.size_tokens
 
+    @_logged("acquire")
     def acquire(self, adapter_id: str, now: TimePoint) -> AcquireResult:
         e = self.entries[adapter_id]
         if not e.resident:
@@ -139,6 +175,7 @@ class AdapterCache:
         self._transition(e, before)
         return AcquireResult(hit=True)
 
+    @_logged("take_ref")
     def take_ref(self, adapter_id: str, now: TimePoint) -> None:
         e = self.entries[adapter_id]
         if not e.resident:
@@ -149,6 +186,7 @@ class AdapterCache:
         e.use_events.append(now)
         self._transition(e, before)
 
+    @_logged("release")
     def release(self, adapter_id: str, now: TimePoint) -> None:
         e = self.entries[adapter_id]
         if e.rc < 1:
@@ -161,6 +199,7 @@ class AdapterCache:
             self._on_drop(e)
         self._transition(e, before)
 
+    @_logged("begin_load")
     def begin_load(self, adapter_id: str, now: TimePoint) -> None:
         e = self.entries[adapter_id]
         if e.resident or e.loading:
@@ -172,6 +211,7 @@ class AdapterCache:
         self._transition(e, before)
         self._on_begin_load(e)
 
+    @_logged("finish_load")
     def finish_load(self, adapter_id: str, now: TimePoint) -> None:
         e = self.entries[adapter_id]
         if not e.loading:
@@ -241,6 +281,7 @@ class AdapterCache:
         self._on_drop(entry)
         return entry.spec.adapter_id
 
+    @_logged("evict_until")
     def evict_until(self, needed_tokens: int, hints: set[str], now: TimePoint) -> list[str]:
         """Evict victims until free >= needed; atomic InsufficientEvictableMemory otherwise."""
         if self.free_tokens >= needed_tokens:
@@ -254,6 +295,7 @@ class AdapterCache:
             out.append(self._evict(self._pick_victim(hints, now)))
         return out
 
+    @_logged("set_capacity")
     def set_capacity(self, tokens: int, hints: set[str], now: TimePoint) -> list[str]:
         """Shrink to `tokens` by eviction; capacity never drops below in-use occupancy."""
         out = []
@@ -266,6 +308,7 @@ class AdapterCache:
         return out
 
     # -- prefetch ---------------------------------------------------------------------------
+    @_logged("note_arrival")
     def note_arrival(self, adapter_id: str, now: TimePoint) -> None:
         if enum_value(self.cfg.prefetch) != PrefetchMode.HISTOGRAM.value:
             return
@@ -280,6 +323,7 @@ class AdapterCache:
             ev.popleft()
         return len(ev)
 
+    @_logged("prefetch_candidates")
     def prefetch_candidates(self, queued_adapter_ids: Iterable[str], free_tokens: int,
                             now: TimePoint) -> list[str]:
         """Queue-driven greedy fit; histogram mode adds top window-arrival adapters."""

@@ -592,7 +592,7 @@ __device__ __forceinline__ void abort_launch(const Params& p) {
 
 __device__ __forceinline__ void trace_producer(const Params& p, int seq, unsigned long long t_it,
                                                unsigned long long t_ready, int kind, uint32_t bytes) {
-  if (p.trace && seq < p.trace_cap) {
+  if (p.trace && seq < p.trace_cap - 1) {
     unsigned long long* tr = p.trace + ((long long)blockIdx.x * p.trace_cap + seq) * 8;
     tr[0] = gtimer();
     tr[1] = ((unsigned long long)kind << 32) | bytes;
@@ -600,8 +600,13 @@ __device__ __forceinline__ void trace_producer(const Params& p, int seq, unsigne
     tr[5] = t_ready;
   }
 }
+// per-CTA life stamps in the last trace slot: 0 entry, 1 plan ready, 2 producer 0 past the
+// PDL wait, 3 consumers done, 4 exit
+__device__ __forceinline__ void trace_cta(const Params& p, int field) {
+  if (p.trace) p.trace[((long long)blockIdx.x * p.trace_cap + p.trace_cap - 1) * 8 + field] = gtimer();
+}
 __device__ __forceinline__ void trace_consumer(const Params& p, int seq, int field) {
-  if (p.trace && seq < p.trace_cap) p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + field] = gtimer();
+  if (p.trace && seq < p.trace_cap - 1) p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + field] = gtimer();
 }
 
 // =========================================================================== K1: shrink
@@ -1471,7 +1476,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
     }
     if (lane == 0) {
       trace_producer(p, seq, t_it, t_ready, 2, bytes);
-      if (p.trace && seq < p.trace_cap) {
+      if (p.trace && seq < p.trace_cap - 1) {
         p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 6] = unit;
         p.trace[((long long)blockIdx.x * p.trace_cap + seq) * 8 + 7] = (np << 8) | tcount;
       }
@@ -1602,10 +1607,12 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Shared& sm = *reinterpret_cast<Shared*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) trace_cta(p, 0);
   if (!prologue(p, sm)) {
     abort_launch(p);
     return;
   }
+  if (tid == 0) trace_cta(p, 1);
   const bool fused = mode == MODE_FUSED;
   // The producer is the highest-numbered warp: the SM's warp schedulers favour higher warp
   // ids, so the producer is never starved by the FMA-heavy consumer warps on its SMSP.
@@ -1693,6 +1700,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     }
   }
   // the last CTA re-arms the unit counters and the tile counters for the next launch
+  if (tid == 0) trace_cta(p, 3);
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -1716,6 +1724,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     }
     __threadfence();
   }
+  if (tid == 0) trace_cta(p, 4);
 }
 
 // One CTA builds the step's plan and writes it to global memory (consumed by every

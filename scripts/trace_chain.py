@@ -63,6 +63,8 @@ def main():
     out = ROOT / "gpurun_out"
     out.mkdir(exist_ok=True)
     np.save(out / f"trace_chain{os.environ.get('TRACE_TAG', '')}.npy", tr)
+    life = tr[:, :, cap - 1, :].copy()  # per-CTA stamps: entry, plan ready, -, consumers done, exit
+    tr = tr[:, :, :cap - 1]
     valid = tr[..., 0] > 0
     t0 = tr[..., 0][valid].min()
     prev_end = None
@@ -88,6 +90,11 @@ def main():
               f"{(cta_first.max() - first_issue) / 1e3:.2f}; CTA end min {cta_end.min() / 1e3:.2f} p10 "
               f"{np.percentile(cta_end, 10) / 1e3:.2f} p50 {np.median(cta_end) / 1e3:.2f}; "
               f"{b / 1e6:.1f} MB -> {b / max(1, last_end - first_issue):.0f} GB/s")
+        ent, pln, dn, ex_ = (life[i, :, j] - t0 for j in (0, 1, 3, 4))
+        print(f"     CTA entry min {ent.min() / 1e3:7.2f} p50 {np.median(ent) / 1e3:7.2f} max {ent.max() / 1e3:7.2f}; "
+              f"plan-ready - entry p50 {np.median(pln - ent) / 1e3:.2f}; exit - consumers-done p50 "
+              f"{np.median(ex_ - dn) / 1e3:.2f} max {(ex_ - dn).max() / 1e3:.2f}; exit min {ex_.min() / 1e3:7.2f} "
+              f"max {ex_.max() / 1e3:7.2f}")
         prev_end = last_end
     span = max(tr[i, :, :, 3][valid[i]].max() for i in range(n_launch)) - t0
     print(f"total {tot_bytes / 1e6:.1f} MB in {span / 1e3:.1f} us -> {tot_bytes / span:.0f} GB/s")
