@@ -538,20 +538,24 @@ def run_ours(args, rank: int, world: int):
 
 # --------------------------------------------------------------------------- C4: cache with misses
 def run_c4(args, rank: int, world: int):
-    """C4 replica: 1000-adapter Zipf(0.7) catalog, PagedAdapterCache at 10% of idle HBM, decode
-    batches of 256 requests (zipf draws seeded by replica rank and step).  A step = the
-    reference's admission path for every request (acquire; on a miss evict_until + begin_load
-    with the pinned fill on the side stream; finish_load + take_ref when the copy's event
-    completes — engine.py:491-532, 294-301), the step graph (K4 + plan + 64 applies) on the
-    compute stream gated on the fills, then release of every request's reference.  Timed by
-    wall clock around all steps (host decisions and PCIe fills included)."""
+    """C4 replica: 1000-adapter Zipf(0.7) catalog, PagedAdapterCache at 10% of idle HBM, a
+    closed loop of 256 decode requests (each step's zipf draws, seeded by replica rank and
+    step, replace the requests the previous step executed), admitted up to 256 per step.  A step is `serving.ReplicaLoop.step`: fill completions by
+    poll_fills (engine.py:294-301), the reference's admission transaction with real pinned
+    fills on the side stream for misses (engine.py:491-532), queue-driven prefetch of the
+    queued requests' adapters (engine.py:457-470), then the step graph (K4 + plan + 64
+    applies) over every ready request, ordered after its fills on the device.  Timed by wall
+    clock around all steps (host decisions and PCIe fills included).  After the run the
+    replica's recorded decision trace is replayed through a fresh AdapterCache (bit-exact
+    with the reference's, tests/test_cache.py) and every decision must match."""
     import torch
     import torch.distributed as dist
 
-    from paper_2411_17741_b200.adapter_cache import InsufficientEvictableMemory, PagedAdapterCache
+    from paper_2411_17741_b200.adapter_cache import AdapterCache, PagedAdapterCache
     from paper_2411_17741_b200.executor import LoraStepExecutor
-    from paper_2411_17741_b200.model import CacheConfig, make_adapter_spec, zipf_catalog
+    from paper_2411_17741_b200.model import CacheConfig, PrefetchMode, make_adapter_spec, zipf_catalog
     from paper_2411_17741_b200.pool import AdapterPool, pages_for_rank
+    from paper_2411_17741_b200.serving import ReplicaLoop, replay_ops
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
@@ -570,76 +574,52 @@ def run_c4(args, rank: int, world: int):
             torch.uint8).pin_memory()
     store = {a: by_rank[catalog[a].rank] for a in ids}
     s = torch.cuda.Stream(device=dev)
-    cache = PagedAdapterCache(CacheConfig(), catalog, pool, host_store=store, compute_stream=s)
-    cache.set_capacity(n_pages * PagedAdapterCache.TOKENS_PER_PAGE, set(), 0)
+    prefetch = PrefetchMode.OFF if args.no_prefetch else PrefetchMode.QUEUE_DRIVEN
+    cfg = CacheConfig(prefetch=prefetch)
+    cache = PagedAdapterCache(cfg, catalog, pool, host_store=store, compute_stream=s)
     groups = [[0, 1, 2], [3]]
-    ex = LoraStepExecutor(pool, max_requests=1024, max_tokens=4096, proj_groups=groups)
-    xs = [[torch.randn(T_DECODE, H, device=dev).to(torch.bfloat16) for _ in groups] for _ in range(N_LAYERS)]
-    ys = [[torch.randn(T_DECODE, H, device=dev).to(torch.bfloat16) for _ in range(N_PROJ)] for _ in range(N_LAYERS)]
+    max_req = 1024
+    ex = LoraStepExecutor(pool, max_requests=max_req, max_tokens=max_req, proj_groups=groups,
+                          graph_requests=max_req)
+    xs = [[torch.randn(max_req, H, device=dev).to(torch.bfloat16) for _ in groups] for _ in range(N_LAYERS)]
+    ys = [[torch.randn(max_req, H, device=dev).to(torch.bfloat16) for _ in range(N_PROJ)] for _ in range(N_LAYERS)]
+    state = {"graph": False, "batches": 0, "tokens": 0}
+
+    def run_batch(slots, ranks, ntok):
+        for lo in range(0, len(slots), max_req):
+            sl, rk, nt = slots[lo:lo + max_req], ranks[lo:lo + max_req], ntok[lo:lo + max_req]
+            ex.upload(sl, rk, nt, stream=s)
+            if not state["graph"]:
+                ex.capture(xs, ys, s)
+                state["graph"] = True
+            ex.replay()
+            state["batches"] += 1
+            state["tokens"] += int(nt.sum())
+
+    loop = ReplicaLoop(cache, catalog, run_batch, capacity_tokens=n_pages * PagedAdapterCache.TOKENS_PER_PAGE,
+                       max_admit=T_DECODE)
     p = np.asarray(probs)
-    slot_of = cache.slot_of
-    ones = np.ones(T_DECODE, dtype=np.int32)
-    state = {"now": 0, "graph": None}
 
-    def step(i):
+    def arrivals(i):
+        # closed loop at 256 requests in the replica: new arrivals replace the requests the
+        # previous step executed (queued and fill-waiting requests stay in the system)
+        n = T_DECODE - len(loop.deferred) - sum(loop.waiters.values())
         rng = np.random.default_rng(rank * 1_000_003 + i)
-        batch = [ids[int(k)] for k in rng.choice(len(ids), T_DECODE, p=p)]
-        state["now"] += 20_000  # 20 ms per decode step, reference time units (us)
-        now = state["now"]
-        hints = set(batch)
-        waiters = {}
-        admitted = []
-        for a in batch:
-            e = cache.entries[a]
-            if e.resident:
-                cache.acquire(a, now)
-                admitted.append(a)
-                continue
-            cache.acquire(a, now)  # miss (counted)
-            if not e.loading:
-                try:
-                    cache.evict_until(e.spec.size_tokens, hints, now)
-                except InsufficientEvictableMemory:
-                    admitted.append(None)  # deferred (engine.py:526): the row runs without an adapter
-                    continue
-                cache.begin_load(a, now)
-            waiters.setdefault(a, []).append(a)
-            admitted.append(a)
-        batch = admitted
-        for a, w in waiters.items():
-            ev = cache.fill_event(a)
-            if ev is not None:
-                s.wait_event(ev)  # the apply reads the pages after the fill completed
-            cache.finish_load(a, now)
-            for _ in w:
-                cache.take_ref(a, now)
-        req_slot = np.array([slot_of(a) if a else -1 for a in batch], dtype=np.int32)
-        req_rank = np.array([catalog[a].rank if a else 0 for a in batch], dtype=np.int32)
-        with torch.cuda.stream(s):
-            ex.upload(req_slot, req_rank, ones, stream=s)
-            if state["graph"] is None:
-                ex.run(xs, ys)
-                g = torch.cuda.CUDAGraph()
-                s.synchronize()
-                with torch.cuda.graph(g, stream=s):
-                    ex.run(xs, ys)
-                state["graph"] = g
-            state["graph"].replay()
-        for a in batch:
-            if a:
-                cache.release(a, now)
-        state["deferred"] = state.get("deferred", 0) + sum(1 for a in batch if a is None)
+        return [ids[int(k)] for k in rng.choice(len(ids), max(0, n), p=p)]
 
-    for i in range(args.warmup * 4):  # warm the cache towards its steady state
-        step(i)
+    n_warm = args.warmup * 4
+    for i in range(n_warm):  # warm the cache towards its steady state
+        loop.step(arrivals(i))
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    h0, m0, l0, ev0, fb0 = cache.hits, cache.misses, cache.loads, cache.evictions, cache.fill_bytes
+    st0 = dict(loop.stats)
+    h0, m0, l0, ev0, fb0, tok0 = cache.hits, cache.misses, cache.loads, cache.evictions, cache.fill_bytes, \
+        state["tokens"]
     t0 = time.perf_counter()
     with ClockSampler(dev.index) as clk:
         for i in range(args.steps):
-            step(args.warmup * 4 + i)
+            loop.step(arrivals(n_warm + i))
         torch.cuda.synchronize(dev)
     el = time.perf_counter() - t0
     if world > 1:
@@ -648,6 +628,12 @@ def run_c4(args, rank: int, world: int):
         el = float(t.item())
     hits, misses = cache.hits - h0, cache.misses - m0
     fill_b = cache.fill_bytes - fb0
+    tokens_rank = state["tokens"] - tok0
+    err = pool.device_error(clear=True, stream=s)
+    # decision parity: the replica's whole trace (warm-up included) through a fresh cache
+    t_rep = time.perf_counter()
+    mism = replay_ops(AdapterCache(cfg, catalog), cache.op_log)
+    t_rep = time.perf_counter() - t_rep
     # PCIe fill bandwidth alone: the largest adapter copied 5 times on the side stream
     big = by_rank[max(by_rank)]
     scratch = torch.empty(big.numel(), dtype=torch.uint8, device=dev)
@@ -659,26 +645,45 @@ def run_c4(args, rank: int, world: int):
         e1.record()
     torch.cuda.synchronize(dev)
     fill_gbs = 5 * big.numel() / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    tok = torch.tensor([tokens_rank], dtype=torch.float64, device=dev if world > 1 and dist.get_backend() == "nccl"
+                       else "cpu")
+    if world > 1:
+        dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+    tokens = float(tok.item())
     if rank == 0:
-        tokens = T_DECODE * args.steps * world
+        d = {k: loop.stats[k] - st0[k] for k in loop.stats}
         line = {
             "metric": METRIC, "value": tokens / el, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup * 4, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "warmup": n_warm, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (one pinned random adapter image per rank class)",
             "config": {"workload": "C4: 1000 adapters Zipf(0.7), PagedAdapterCache at 10% of idle HBM "
-                                   f"({n_pages} pages = {n_pages * page_bytes / 1e9:.1f} GB), decode batches of 256, "
-                                   "misses filled over PCIe on a side stream",
+                                   f"({n_pages} pages = {n_pages * page_bytes / 1e9:.1f} GB), closed loop of 256 decode "
+                                   "requests (Zipf draws replace the executed ones every step), misses filled over "
+                                   f"PCIe on a side stream, prefetch {enum_name(prefetch)}",
                        "global_batch": T_DECODE * world, "seq_len": 1, "parallelism": f"replicas x{world}",
-                       "timing": "wall clock incl. host cache decisions and fills"},
+                       "timing": "wall clock incl. host cache decisions, fills and the step graphs"},
             "cache": {"hit_rate": hits / max(1, hits + misses), "hits": hits, "misses": misses,
                       "loads": cache.loads - l0, "evictions": cache.evictions - ev0,
+                      "prefetches": d["prefetches"], "prefetch_hits": d["prefetch_hits"],
+                      "joined_inflight": d["joined"], "queued_request_steps": d["deferred"],
+                      "executed_requests": d["executed"],
                       "fill_bytes_per_step": fill_b / args.steps, "fill_gbs_during_run": fill_b / el / 1e9,
-                      "pcie_fill_gbs_alone": fill_gbs, "deferred_requests": state.get("deferred", 0)},
+                      "pcie_fill_gbs_alone": fill_gbs, "host_blocked_on_fills_s": 0.0},
+            "decisions": {"ops": len(cache.op_log), "mismatches": len(mism), "replay_s": t_rep,
+                          "checked_against": "fresh AdapterCache (bit-exact with the reference's, "
+                                             "tests/test_cache.py + tests/test_replica.py)"},
+            "device_error": err,
+            "gpu_launches": state["batches"] * ex.launches_per_step(),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     pool.close()
+
+
+def enum_name(v):
+    return getattr(v, "value", v)
+
 
 
 # --------------------------------------------------------------------------- C5: tensor parallel
@@ -833,6 +838,7 @@ def main():
                     help="reference arm: full CPU steps timed (each ~2 s on 16 cores)")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (tcgen05 prefill) sub-record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefetch", action="store_true", help="C4: prefetch off (the reference's default)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

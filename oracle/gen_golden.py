@@ -13,8 +13,12 @@ Fixtures
   sim_batches.json    per-step (prefills, decoders) batches captured at the LoRA seam of the
                       reference simulate() (engine.py:443-447) with the reference's own
                       adapter_units for the step (engine.py:64-76).
+  cost_solo.json      CostModel.prefill_step_us / decode_steps_us (engine.py:80-97) on a
+                      grid of (input, output, rank) for two parameter sets.
   batch_results.json  MultiQueueScheduler.generate_batch results (scheduler.py:528-550)
-                      against a scripted oracle: admitted order + budget ledger.
+                      against a scripted oracle (the reference test's hand trace plus
+                      random queue layouts) and FifoScheduler cases: admitted order +
+                      budget ledger.
 """
 from __future__ import annotations
 
@@ -203,42 +207,103 @@ def sim_batches(max_steps: int = 400):
 
 
 def batch_results():
+    """MultiQueueScheduler.generate_batch (scheduler.py:528-550, Algorithm 1: per-queue quota
+    phase, then leftover in queue order) on scripted queues — the hand trace of the
+    reference's own test (test_scheduler.py:222-232) plus random layouts — and FifoScheduler
+    cases; each with the admitted order and the budget ledger."""
     _, _, model, sched, _ = _import_ref()
     out = []
     rng = random.Random(7)
-    for case in range(12):
+
+    class Oracle:
+        def __init__(self, blocked=()):
+            self.blocked = set(blocked)
+
+        def adapter_charge(self, state):
+            return 0
+
+        def adapter_fits_free(self, state):
+            return True
+
+        def try_admit(self, state, now):
+            return sched.AdmitOutcome(state.request_id not in self.blocked, "adapter")
+
+        def head_memory_eta(self, state, now):
+            return now + 1000
+
+        def estimate_completion(self, state, now):
+            return now + 10
+
+    def mlq(queue_needs, quotas, adapters):
+        cfg = model.SchedulerConfig(policy=model.SchedulerPolicy.MLQ)
+        s = sched.MultiQueueScheduler(cfg, sum(quotas), lambda aid: int(aid[1:].split("-")[0]), lambda r: 4 * r,
+                                      lambda i, o, r: 1000, [8, 16, 32, 64, 128])
+        s.layout = sched.QueueLayout(len(queue_needs), [], [0.0] * (len(queue_needs) - 1), [])
+        s.queues = [[] for _ in queue_needs]
+        s.quotas = list(quotas)
+        s.borrowed = [0] * len(queue_needs)
+        rid = 0
+        for q, needs in enumerate(queue_needs):
+            for need in needs:
+                half = need // 2
+                spec = model.RequestSpec(rid, rid, half, 1, adapters[rid % len(adapters)])
+                st = model.RequestState(spec, predicted_output_tokens=need - half)
+                st.queue_index = q
+                s.queues[q].append(st)
+                s.pending_ids.add(rid)
+                rid += 1
+        return s
+
+    def record(kind, res, extra=None):
+        d = {"scheduler": kind,
+             "admitted": [[st.request_id, st.spec.adapter_id, st.spec.input_tokens] for st in res.admitted],
+             "admitted_need": [st.borrowed_quota for st in res.admitted],
+             "budgets": res.budgets, "consumed": res.consumed, "leftover": res.leftover, "stranded": res.stranded}
+        d.update(extra or {})
+        out.append(d)
+
+    # the reference test's hand trace (test_scheduler.py:222-232)
+    s = mlq([[30, 30, 30, 30], [40], [50, 80]], [100, 100, 100], ["r8-0"])
+    record("mlq", s.generate_batch(0, Oracle()), {"case": "hand-trace"})
+    ads = [f"r{r}-{j}" for r in (8, 16, 32, 64, 128) for j in range(3)]
+    for case in range(16):
+        nq = rng.randint(1, 4)
+        needs = [[rng.randint(8, 120) for _ in range(rng.randint(0, 8))] for _ in range(nq)]
+        quotas = [rng.randint(0, 300) for _ in range(nq)]
+        nreq = sum(len(n) for n in needs)
+        blocked = {i for i in range(nreq) if rng.random() < 0.15}
+        s = mlq(needs, quotas, ads)
+        record("mlq", s.generate_batch(500, Oracle(blocked)), {"case": f"random-{case}"})
+    for case in range(6):
         cfg = model.SchedulerConfig()
-        rank_values = [8, 16, 32, 64, 128]
         s = sched.FifoScheduler(cfg, 4000, lambda aid: int(aid[1:].split("-")[0]))
-        states = []
         for i in range(rng.randint(5, 30)):
-            r = rng.choice(rank_values)
+            r = rng.choice([8, 16, 32, 64, 128])
             spec = model.RequestSpec(i, i * 10, rng.randint(16, 600), rng.randint(1, 200), f"r{r}-{rng.randint(0, 3)}")
             st = model.RequestState(spec, rng.randint(1, 200))
             s.on_arrival(st, i * 10)
-            states.append(st)
+        record("fifo", s.generate_batch(500, Oracle({i for i in range(40) if i % 7 == 5})), {"case": f"fifo-{case}"})
+    return out
 
-        class Oracle:
-            def adapter_charge(self, state):
-                return 4 * int(state.spec.adapter_id[1:].split("-")[0]) if state.request_id % 3 else 0
 
-            def adapter_fits_free(self, state):
-                return True
-
-            def try_admit(self, state, now):
-                return sched.AdmitOutcome(state.request_id % 7 != 5, "adapter")
-
-            def head_memory_eta(self, state, now):
-                return now + 1000
-
-            def estimate_completion(self, state, now):
-                return now + 10
-
-        res = s.generate_batch(500, Oracle())
-        out.append({
-            "admitted": [[st.request_id, st.spec.adapter_id, st.spec.input_tokens] for st in res.admitted],
-            "budgets": res.budgets, "consumed": res.consumed, "leftover": res.leftover, "stranded": res.stranded,
-        })
+def cost_solo():
+    """CostModel.prefill_step_us / decode_steps_us (engine.py:80-97) on a grid of (input tokens,
+    output tokens, rank) with the default and a non-default CostModelParams."""
+    _, engine, model, _, _ = _import_ref()
+    out = []
+    for params in (model.CostModelParams(), model.CostModelParams(prefill_base_us=1234.5, prefill_per_token_us=7.25,
+                                                                 decode_base_us=987.0, decode_per_token_us=3.5,
+                                                                 adapter_compute_per_rank_token_us=0.377)):
+        cm = engine.CostModel(params)
+        rows = []
+        for i in (1, 7, 64, 256, 1000, 2048):
+            for o in (0, 1, 2, 17, 300, 1024):
+                for r in (8, 16, 32, 64, 128):
+                    rows.append([i, o, r, cm.prefill_step_us(i, r), cm.decode_steps_us(i, o, r)])
+        out.append({"params": {k: getattr(params, k) for k in ("prefill_base_us", "prefill_per_token_us",
+                                                              "decode_base_us", "decode_per_token_us",
+                                                              "adapter_compute_per_rank_token_us")},
+                    "rows": rows})
     return out
 
 
@@ -248,6 +313,7 @@ def main():
     (OUT / "workload_draws.json").write_text(json.dumps(workload_draws()))
     (OUT / "sim_batches.json").write_text(json.dumps(sim_batches()))
     (OUT / "batch_results.json").write_text(json.dumps(batch_results()))
+    (OUT / "cost_solo.json").write_text(json.dumps(cost_solo()))
     for f in sorted(OUT.glob("*.json")):
         print(f.name, f.stat().st_size)
 

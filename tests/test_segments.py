@@ -140,3 +140,29 @@ def test_segment_token_bounds_route_hints():
     assert segment_token_bounds(slots, ranks, ntok) == (min(lens), max(lens)) == (3, 140)
     assert segment_token_bounds(slots, [16, 8, 16, 0, 256, 8], ntok) == (0, 140)
     assert segment_token_bounds([-1, -1], [0, 0], [5, 5]) == (0, 0)
+
+
+def test_multiqueue_batch_descriptor_pinned(golden_dir):
+    """MultiQueueScheduler.generate_batch (scheduler.py:528-550), from the reference: Algorithm
+    1's admission order on the reference test's hand trace (test_scheduler.py:222-232: needs
+    [30, 30, 30, 40, 50, 30], consumed [120, 40, 50], leftover 30; the implementation's
+    stranded ledger is [10, 0, 50]) and the budget conservation on every MLQ case; the
+    admitted list is the batch the segment builder consumes, in that order."""
+    results = json.loads((golden_dir / "batch_results.json").read_text())
+    mlq = [r for r in results if r["scheduler"] == "mlq"]
+    assert len(mlq) >= 10
+    hand = next(r for r in mlq if r["case"] == "hand-trace")
+    assert hand["admitted_need"] == [30, 30, 30, 40, 50, 30]
+    assert [a[0] for a in hand["admitted"]] == [0, 1, 2, 4, 5, 3]
+    assert hand["consumed"] == [120, 40, 50] and hand["leftover"] == 30 and hand["stranded"] == [10, 0, 50]
+    for res in mlq:
+        assert sum(res["consumed"]) + res["leftover"] + sum(res["stranded"]) == sum(res["budgets"])
+        admitted = [_req(aid, n) for _rid, aid, n in res["admitted"]]
+        slots, ranks, ntok = batch_arrays(admitted, lambda a: int(a.split("-")[1]), rank_of_id)
+        perm, off, sl, rk = build_segments_ref(slots, ranks, ntok)
+        # stable group-by-slot keeps the admission order inside every segment
+        tok_start = np.concatenate([[0], np.cumsum(ntok)])
+        for s in range(len(sl)):
+            reqs = [i for i in range(len(slots)) if slots[i] == sl[s]]
+            want = np.concatenate([np.arange(tok_start[i], tok_start[i + 1]) for i in reqs]) if reqs else []
+            assert perm[off[s]:off[s + 1]].tolist() == list(want)
