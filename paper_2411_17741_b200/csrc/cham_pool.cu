@@ -169,6 +169,7 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_vws);
     cudaFree(pool->d_plan);
     cudaFree(pool->d_pvimg);
+    cudaFree(pool->d_ppart);
     cudaFree(pool->d_pctr);
     cudaFree(pool->d_split);
     cudaFree(pool->d_split_ctr);
@@ -208,6 +209,8 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
   if (e == cudaSuccess) e = cudaMemset(pool->d_split_ctr, 0, 2 * n_split * sizeof(int));
   if (e == cudaSuccess && pool->prefill_ok)
     e = cudaMalloc(&pool->d_pvimg, (size_t)kMaxJobs * kPrefillMaxTiles * kPrefillVImg);
+  if (e == cudaSuccess && pool->prefill_ok)
+    e = cudaMalloc(&pool->d_ppart, (size_t)kMaxJobs * kPrefillMaxTiles * kPrefillPart);
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMalloc(&pool->d_pctr, sizeof(int) * prefill_ctr_ints());
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMemset(pool->d_pctr, 0, sizeof(int) * prefill_ctr_ints());
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
@@ -231,6 +234,7 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_vws);
   cudaFree(pool->d_plan);
   cudaFree(pool->d_pvimg);
+  cudaFree(pool->d_ppart);
   cudaFree(pool->d_pctr);
   cudaFree(pool->d_split);
   cudaFree(pool->d_split_ctr);

@@ -38,7 +38,8 @@ struct cham_pool {
   int prefill_min_tokens = 0;          // 0 = tcgen05 path disabled
   int route_min_seg = 0;               // host hints about the next steps' segment lengths
   int route_max_seg = 1 << 30;
-  char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB] (ks partials)
+  char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB] (bf16, one per tile)
+  float* d_ppart = nullptr;            // prefill split-K fp32 partials [kMaxJobs][kPrefillMaxTiles][64 KiB]
   int* d_pctr = nullptr;               // prefill counters: 2 parity sets + tile V flags
   int prefill_epoch = 0;               // prefill launches so far (tile flags, counter parity)
   float* d_split = nullptr;            // decode page-half partials [kMaxJobs][kSplitCap][split_ncc][4][2048 B cols]
@@ -58,7 +59,9 @@ constexpr int kPrefillMinTokens = 64;  // default routing threshold (segment tok
 constexpr int kPrefillMaxRank = 128;   // largest rank on the tcgen05 path (TMEM / smem budget)
 constexpr int kPrefillMaxSplit = 8;    // shrink split-K factor bound (workspace sizing)
 constexpr int kPrefillMaxTiles = 256;  // 128-row prefill tiles per apply (workspace sizing)
-constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles;  // one parity set: dispatch, done, spare, tile counters
+constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles + kPrefillMaxTiles * cham::kMaxJobs;  // one parity set:
+// dispatch, done, spare x2, tile V counters [tiles], split-K arrival counters [tiles][groups]
+constexpr size_t kPrefillPart = 65536;                 // fp32 split-K partial bytes per (job, tile)
 constexpr size_t kPrefillVImg = 32768;                // V image bytes per (job, tile)
 inline size_t prefill_ctr_ints() { return 2 * kPrefillCtrSet + kPrefillMaxTiles; }
 

@@ -52,19 +52,36 @@ constexpr int VBUF = CHAM_PF_VBUF;      // V images of one (job, tile): ks parti
 #ifndef CHAM_PF_PDL
 #define CHAM_PF_PDL 1  // programmatic dependent launch for the prefill kernel
 #endif
+#ifndef CHAM_PF_YREG
+#define CHAM_PF_YREG 1  // expand y path: 1 = epilogue registers (ld/st.global, ring stages carry B only), 0 = y rows staged in the ring
+#endif
+constexpr bool kYReg = CHAM_PF_YREG != 0;
+#ifndef CHAM_PF_YPF
+#define CHAM_PF_YPF 1  // register y path: L2 prefetch of the set's later groups at unit start
+#endif
+constexpr bool kYPrefetch = CHAM_PF_YPF != 0;
 #ifndef CHAM_PF_CW
 #define CHAM_PF_CW 256  // expand unit width; A/B on C3: 256 -> 642k, 512 -> 625k, 1024 -> 553k tok/s
 #endif
 constexpr int CW = CHAM_PF_CW;          // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
+#ifndef CHAM_PF_CD
+#define CHAM_PF_CD 1  // outstanding unit claims per loader (A/B on C3: 1 -> 590k, 4 -> 347k tok/s: early claims of expand units block on unready tiles)
+#endif
+constexpr int CD = CHAM_PF_CD;
 constexpr int MAX_TILES = kPrefillMaxTiles;
 constexpr int NTHREADS = 384;           // warps 0-7 epilogue (two sets of 4), 8 loader, 9 MMA, 10-11 publishers
 constexpr int W_LOAD = 8, W_MMA = 9, W_PUB = 10;
 constexpr int PQN = 8;                  // publish ring depth per epilogue set
 constexpr int TMEM_COLS = 512;
-constexpr int TM_SH = 192;              // shrink accumulator stride: [0,192) and [192,384)
-constexpr int TM_EX = 384;              // expand accumulators: [384,448) and [448,512)
+// TMEM: two shrink accumulators of TM_SH columns, then NACC expand accumulators of 64 columns
+// (register-y path: 2 x 128 + 4 x 64, so four expand groups are in flight between the MMA
+// warp and the epilogue; staged-y path: 2 x 192 + 2 x 64)
+constexpr int NACC = CHAM_PF_YREG ? 4 : 2;
+constexpr int TM_SH = CHAM_PF_YREG ? 128 : 192;
+constexpr int TM_EX = 2 * TM_SH;
+static_assert(TM_EX + NACC * 64 <= TMEM_COLS, "TMEM budget");
 constexpr int BAR_EPI = 1;              // named barriers 1, 2: the 128 threads of epilogue set 0, 1
 
 enum Mode { MODE_FUSED = 0, MODE_SHRINK = 1, MODE_EXPAND = 2 };
@@ -101,7 +118,9 @@ struct alignas(64) Params {
   int thr;                 // routing threshold (segment tokens)
   int epoch;               // launch id (tile V flags), parity selects the counter set
   int* ctr;                // this parity's counters: [0] dispatch, [1] finished CTAs, [2] error
-  int* tile_cnt;           // this parity's split-K arrival counters [MAX_TILES]
+  int* tile_cnt;           // this parity's tile counters [MAX_TILES]: reduced V images published
+  int* arrive;             // this parity's split-K arrival counters [MAX_TILES][kMaxJobs] (tile, job group)
+  float* ppart;            // fp32 split-K partials [job][tile][kPrefillPart / 4]
   int* err;
   char* vimg;              // V images [job][tile][VBUF]
   float* v_out;            // MODE_SHRINK: v [position][v_stride]
@@ -231,6 +250,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void trace_put(const Params& p, int k, int field, unsigned long long v) {
   if (p.trace && k < p.trace_cap) p.trace[((long long)blockIdx.x * p.trace_cap + k) * 8 + field] = v;
 }
+// loader detail timeline (debug): the first half of the debug buffer (the decode kernel's,
+// unused while a prefill-only chain runs): 0 unit ring slot free, 1 next unit id known, 2 V
+// buffer free, 3 tile ready, 4 V copy issued, 5 first ring stage free
+__device__ __forceinline__ void trace_ld(const Params& p, int k, int field) {
+  if (p.trace && k < p.trace_cap)
+    p.trace[(((long long)blockIdx.x - (long long)gridDim.x) * p.trace_cap + k) * 8 + field] = gtimer();
+}
 // debug breadcrumbs of the CTA's own progress (trace builds only): slot trace_cap - 1,
 // written by thread 0 and pushed to memory at system scope (the trace may be host-mapped)
 __device__ __forceinline__ void crumb(const Params& p, int field, unsigned long long v) {
@@ -344,7 +370,8 @@ __host__ __device__ __forceinline__ int rpad(int rank) { return (rank + 15) & ~1
 __host__ __device__ __forceinline__ int mpad(int m) { return (m + 63) & ~63; }  // 64-row TMA boxes
 // jobs sharing one shrink stage: all of them when their A^T atoms fit a 16 KiB region
 __device__ __forceinline__ int jobs_per_group(const Params& p, int rank) {
-  return (p.mode == MODE_FUSED && p.x_shared && p.n_jobs * (rpad(rank) / 8) <= 16) ? p.n_jobs : 1;
+  return (p.mode == MODE_FUSED && p.x_shared && p.n_jobs * (rpad(rank) / 8) <= 16 && p.n_jobs * rpad(rank) <= TM_SH)
+             ? p.n_jobs : 1;
 }
 __device__ __forceinline__ int n_groups(const Params& p, int rank) { return p.n_jobs / jobs_per_group(p, rank); }
 
@@ -404,8 +431,8 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
     int u = 0;
     if (t < tiles) {
       int kt = ks;
-      const int img = ((rpad(tl.t[t].rank) + 63) / 64) * mpad(tl.t[t].m) * 128;
-      while (kt > 1 && kt * img > VBUF) kt >>= 1;
+      const int part = mpad(tl.t[t].m) * rpad(tl.t[t].rank) * 4;  // one K range's fp32 partial
+      while (kt > 1 && kt * part > (int)kPrefillPart) kt >>= 1;
       tl.t[t].ks = kt;
       u = p.mode == MODE_EXPAND ? 1 : kt * n_groups(p, tl.t[t].rank);
     }
@@ -447,8 +474,8 @@ struct Unit {
   int ngrp;           // expand: 64-column groups in the unit
   int kpc, nst;       // chunks (shrink) / groups (expand) per stage, stages
   int nchunks;        // shrink: k-chunks in the unit
-  int ks;             // the tile's K-split (expand: partial V images to accumulate)
-  int vstride;        // bytes of one partial V image (K-blocks x mp rows x 128 B)
+  int ks;             // the tile's shrink K-split (fp32 partials reduced into ONE V image)
+  int vstride;        // bytes of the tile's V image (K-blocks x mp rows x 128 B)
   int xb;             // bytes of one activation chunk/group in smem (mp rows x 128 B)
   int bstride;        // expand: bytes of one group's B slices (np rounded up to even, x 1 KiB)
 };
@@ -490,7 +517,7 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
     x.nst = (x.nchunks + x.kpc - 1) / x.kpc;
   } else if (x.kind == 2) {
     x.ngrp = min(NGRP, (p.h_out - x.col0) / 64);
-    x.kpc = max(1, min(4, STAGE / (x.bstride + x.xb)));
+    x.kpc = kYReg ? max(1, min(NGRP, STAGE / x.bstride)) : max(1, min(4, STAGE / (x.bstride + x.xb)));
     x.nst = (x.ngrp + x.kpc - 1) / x.kpc;
   } else {
     x.kpc = 0;
@@ -508,19 +535,24 @@ struct Prefetch {
   int page;     // lane l < np: pool page l of the adapter
 };
 __device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileList& tl, int u_id, int lane) {
+  // Every load is unconditional (clamped to a valid unit): the values are consumed one unit
+  // later, and a predicated load merged with a default would make the loader wait for it now.
   Prefetch f;
-  f.page = 0;
+  if (tl.u_total == 0) {  // no prefill work in this apply
+    f.page = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) f.rows[b] = 0;
-  if (u_id < 0 || u_id >= tl.u_total || (u_id < tl.u1 && p.mode == MODE_EXPAND)) return f;
-  const Tile& t = tl.t[u_id < tl.u1 ? tile_of_unit(tl, u_id)
-                                    : (u_id - tl.u1) / (p.n_jobs * ((p.h_out + CW - 1) / CW))];
-  const int np = (t.rank + 7) / 8;
-  if (lane < np) f.page = __ldg(p.slot_pages + t.slot * kMaxPagesPerSlot + lane);
+    for (int b = 0; b < 4; ++b) f.rows[b] = 0;
+    return f;
+  }
+  const bool ok = u_id >= 0 && u_id < tl.u_total;
+  const int uu = ok ? u_id : 0;
+  const int ti = uu < tl.u1 ? tile_of_unit(tl, uu) : (uu - tl.u1) / (p.n_jobs * ((p.h_out + CW - 1) / CW));
+  const Tile& t = tl.t[ti];
+  f.page = __ldg(p.slot_pages + t.slot * kMaxPagesPerSlot + min(lane, kMaxPagesPerSlot - 1));
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
     const int pos = t.pos0 + min(b * 32 + lane, t.m - 1);
-    if (b * 32 < t.m) f.rows[b] = p.perm ? __ldg(p.perm + pos) : pos;
+    f.rows[b] = p.perm ? __ldg(p.perm + pos) : pos;
   }
   return f;
 }
@@ -528,8 +560,13 @@ __device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileLis
 #define CHAM_WARM_L2 0  // A/B on C3: 461.7k (on) vs 520.8k tok/s (off)
 #endif
 constexpr bool kWarmL2 = CHAM_WARM_L2 != 0;
+#ifndef CHAM_PF_WARM_Y
+#define CHAM_PF_WARM_Y 0  // 1: (A/B on C3: 592k vs 635k tok/s off) the loader pulls an expand unit's y rows into L2 when it claims the unit
+#endif
+constexpr bool kWarmY = CHAM_PF_WARM_Y != 0 && CHAM_PF_YREG != 0;
 #ifndef CHAM_EXP_NOEPI
-#define CHAM_EXP_NOEPI 0  // experiment builds only: the expand epilogue skips the y update
+#define CHAM_EXP_NOEPI 0  // experiment builds only: 1 the expand epilogue skips the y update (stores), 2 also
+                          // the y loads, 3 also the accumulator reads (released unread)
 #endif
 constexpr bool kNoEpi = CHAM_EXP_NOEPI != 0;
 #ifndef CHAM_PF_CHECK
@@ -595,7 +632,7 @@ struct Shared {
   // never overlaps the other buffer, which the loader may be filling (TMA) at the same time.
   alignas(1024) unsigned char vbuf[2][VBUF + VPAD];
   uint64_t full[NS], empty[NS];
-  uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[2], tempty_ex[2];
+  uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[NACC], tempty_ex[NACC];
   uint64_t vfull[2], vempty[2];
   uint64_t drain;  // the MMA warp's last commit: every earlier commit arrival has landed
   uint64_t ufull[UQ], uempty[UQ];
@@ -603,6 +640,7 @@ struct Shared {
   uint32_t tmem_base;
   int last[2];
   int flag;
+  int last_arr[2];  // epilogue set es: its shrink unit was the tile group's last split-K arrival
   // epilogue set es -> publisher warp W_PUB + es: finished shrink units / V images
   int pq_tile[2][PQN];
   int pq_kind[2][PQN];  // 0 end, 1 split-K partials written (count, last one reduces), 2 V written
@@ -616,6 +654,10 @@ static_assert(sizeof(Shared) <= 227 * 1024, "prefill kernel shared memory exceed
 // b * mp*128 + r*128 + ((c ^ r) & 7) * 16 — the K-major SWIZZLE_128B A-operand layout.
 __device__ __forceinline__ char* vimg_of(const Params& p, int job, int tile) {
   return p.vimg + ((long long)job * MAX_TILES + tile) * VBUF;
+}
+// fp32 split-K partials of (job, tile): [kq][mp rows][rp ranks]
+__device__ __forceinline__ float* part_of(const Params& p, int job, int tile) {
+  return p.ppart + ((size_t)job * MAX_TILES + tile) * (kPrefillPart / sizeof(float));
 }
 // ranks [c0, c0 + 32) of row r (v[i] = rank c0 + i; ranks >= nvals are written as zero),
 // clipped to the rp columns of the image
@@ -634,6 +676,8 @@ __device__ __forceinline__ void write_v_chunk(char* img, const Unit& u, int r, i
     }
   }
 }
+
+__device__ __forceinline__ bool s_first_group_ok(int g0, int ngrp) { return g0 < ngrp; }
 
 // Epilogue set -> its publisher warp.  The set's partial / V stores precede the post through
 // the set's named barrier (CTA-scope ordering) and the release of pq_full; the publisher's
@@ -685,10 +729,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull_sh[i], 1);
       mbar_init(&sm.tempty_sh[i], 4);
-      mbar_init(&sm.tfull_ex[i], 1);
-      mbar_init(&sm.tempty_ex[i], 4);
+
       mbar_init(&sm.vfull[i], 1);
       mbar_init(&sm.vempty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&sm.tfull_ex[i], 1);
+      mbar_init(&sm.tempty_ex[i], 4);
     }
     mbar_init(&sm.drain, 1);
     for (int i = 0; i < UQ; ++i) {
@@ -731,17 +778,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     const uint64_t pol_w = policy_evict_first();  // adapter pages: streamed
     const uint64_t pol_x = CHAM_PF_XPOL_NORMAL == 1 ? policy_evict_normal() : CHAM_PF_XPOL_NORMAL == 2 ? policy_evict_first() : policy_evict_last();  // x: re-read by the other job groups / K ranges
     const uint64_t pol_y = policy_evict_first();
-    int next = blockIdx.x;  // first unit static, the rest from the counter (one claim ahead)
-    int claim = 0;
-    if (lane == 0 && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
+    // first unit static, the rest from the counter: lanes 0 .. CD-1 each hold one outstanding
+    // claim (consumed round-robin and refilled at once), so a unit's id never waits for the
+    // atomic's round trip
+    int next = blockIdx.x;
+    int claim = 1 << 29, chead = 0;
+    if (lane < CD && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
     // published phase-1 units of an expand unit's tile, read without blocking one unit ahead
     const int ex_per_tile = p.n_jobs * ((p.h_out + CW - 1) / CW);
-    auto peek_flag = [&](int u) {
-      int v = 0;
-      if (lane == 0 && u >= tl.u1 && u < tl.u_total) {
-        const int* f = p.tile_cnt + (u - tl.u1) / ex_per_tile;
-        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      }
+    auto peek_flag = [&](int u) {  // unconditional (clamped) load: the value is used one unit later
+      int v;
+      const int* f = p.tile_cnt + min(max(u - tl.u1, 0) / ex_per_tile, MAX_TILES - 1);
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       return v;
     };
     int flag = peek_flag(next);
@@ -757,14 +805,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         if (k >= UQ) pf_wait(p, &sm.uempty[q], ((k / UQ) - 1) & 1, 3, k, 0);
         sm.uslot[q] = u_id;
         mbar_arrive(&sm.ufull[q]);
+        trace_ld(p, k, 0);
       }
       if (u_id < 0) break;
-      next = __shfl_sync(0xffffffffu, claim, 0) + gridDim.x;
-      if (lane == 0 && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
+      // The next unit's claim and its lookahead loads (tile counter peek, page ids, token
+      // rows); their values are consumed one unit later.  (Issuing them after the expand
+      // unit's acquire fence instead: A/B on C3 588k vs 600k tok/s.)
       const int cur_flag = flag;
-      flag = peek_flag(next);
       const Prefetch cf = pf;
-      pf = prefetch_unit(p, tl, next, lane);
+      auto advance = [&]() {
+        // the lanes' claims were issued together, so their order is not the counter's; an
+        // exhausted claim (>= the unit count) is skipped until every lane's is
+        for (;;) {
+          const int h = chead;
+          chead = chead + 1 == CD ? 0 : chead + 1;
+          next = __shfl_sync(0xffffffffu, claim, h) + gridDim.x;
+          if (next < tl.u_total) {
+            if (lane == h) claim = atomicAdd(p.ctr, 1);
+            break;
+          }
+          if (lane == h) claim = 1 << 29;
+          if (!__any_sync(0xffffffffu, lane < CD && claim + (int)gridDim.x < tl.u_total)) break;
+        }
+        if (lane == 0) trace_ld(p, k, 1);
+        flag = peek_flag(next);
+        pf = prefetch_unit(p, tl, next, lane);
+      };
+      advance();
       const Unit u = make_unit(p, tl, u_id);
       if (lane == 0 && p.trace) {
         trace_put(p, k, 0, gtimer());
@@ -833,18 +900,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         const int vb = nex & 1;
         if (lane == 0) {
           if (nex >= 2) pf_wait(p, &sm.vempty[vb], ((nex >> 1) - 1) & 1, 5, nex, u_id);
+          trace_ld(p, k, 2);
           // every phase-1 unit of the tile has published its partial V image
-          const int need = tl.sh_start[u.tile + 1] - tl.sh_start[u.tile];
+          const int need = p.mode == MODE_EXPAND ? 1 : n_groups(p, u.rank);  // reduced images of the tile
           if (cur_flag < need) {
             while (ld_acquire_gpu(p.tile_cnt + u.tile) < need) __nanosleep(32);
           } else if (!CHAM_PF_NOACQ) {
             fence_acquire_gpu();  // the relaxed peek saw the count: acquire pattern before the V read
           }
           fence_proxy_async_global();
-          const uint32_t vbytes = u.ks * u.vstride;
+          trace_ld(p, k, 3);
+          const uint32_t vbytes = u.vstride;
           PF_CHECK(vbytes <= VBUF && vbytes > 0 && u.tile < tl.n_tiles && u.job < p.n_jobs, 6, vbytes, u.tile);
           mbar_arrive_expect_tx(&sm.vfull[vb], vbytes);
           bulk_g2s(sm.vbuf[vb], vimg_of(p, u.job, u.tile), vbytes, &sm.vfull[vb], pol_w);
+          trace_ld(p, k, 4);
         }
         __syncwarp();
         ++nex;
@@ -861,6 +931,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           const int ng = min(u.kpc, u.ngrp - g_first);
           if (seq >= NS) pf_wait(p, &sm.empty[st], ((seq / NS) - 1) & 1, 6, seq, u_id);
           if (s == 0 && lane == 0 && p.trace) trace_put(p, k, 7, gtimer());
+          if (s == 0 && lane == 0) trace_ld(p, k, 5);
           unsigned char* stg = sm.ring[st];
           if (pad) {
             // odd page count: the K rows rank..rp of every group are a zero atom (page np)
@@ -870,10 +941,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           }
           __syncwarp();
           uint32_t bytes = ng * u.np * kAtomBytes;
+          if (!kYReg) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (h * 64 < u.m) bytes += ng * (c64[h] ? 64 * 128 : min(64, u.m - h * 64) * 128);
-          PF_CHECK(bytes <= STAGE && u.kpc * u.bstride + ng * u.xb <= STAGE && ng > 0, 7, bytes, ng);
+            for (int h = 0; h < 2; ++h)
+              if (h * 64 < u.m) bytes += ng * (c64[h] ? 64 * 128 : min(64, u.m - h * 64) * 128);
+          }
+          PF_CHECK(bytes <= STAGE && u.kpc * u.bstride + (kYReg ? 0 : ng * u.xb) <= STAGE && ng > 0, 7, bytes, ng);
           PF_CHECK(u.col0 / 64 + g_first + ng <= p.h_out / 64, 8, u.col0, g_first);
           PF_CHECK(lane >= u.np || (my_page >= 0 && my_page < p.n_pages), 9, my_page, u.slot);
 #pragma unroll
@@ -886,7 +959,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
                               (long long)(u.col0 / 64 + g_first) * kAtomBytes;
             bulk_g2s(stg + lane * u.kpc * kAtomBytes, src, ng * kAtomBytes, &sm.full[st], pol_w);
           }
-          for (int g = 0; g < ng; ++g) {
+          for (int g = 0; g < (kYReg ? 0 : ng); ++g) {
             const int col = u.col0 + (g_first + g) * 64;
             unsigned char* ydst = stg + u.kpc * u.bstride + g * u.xb;
 #pragma unroll
@@ -984,24 +1057,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           tc_fence_after();
           const uint32_t base = smem_u32(sm.ring[st]);
           for (int g = 0; g < ng; ++g, ++ngrp) {
-            const int acc = ngrp & 1;
-            if (ngrp >= 2) pf_wait(p, &sm.tempty_ex[acc], ((ngrp >> 1) - 1) & 1, 12, ngrp, u_id);
+            const int acc = ngrp % NACC;
+            if (ngrp >= NACC) pf_wait(p, &sm.tempty_ex[acc], ((ngrp / NACC) - 1) & 1, 12, ngrp, u_id);
             tc_fence_after();
             if (lane == 0) {
               const uint32_t ba = base + g * kAtomBytes;  // B atoms [page][group]
-              // D2 = sum over the tile's K-split partial images V_kq of V_kq . B
-              for (int kq = 0; kq < u.ks; ++kq)
-                for (int kk = 0; kk < u.rp / 16; ++kk) {
-                  const uint64_t ad = sdesc(va + kq * u.vstride + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
-                  const uint64_t bd = sdesc(ba + kk * 2 * u.kpc * kAtomBytes, kAtomBytes, u.kpc * kAtomBytes);
-                  mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, (kq | kk) ? 1u : 0u);
-                }
+              // D2 = V . B over the tile's (reduced) V image
+              for (int kk = 0; kk < u.rp / 16; ++kk) {
+                const uint64_t ad = sdesc(va + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
+                const uint64_t bd = sdesc(ba + kk * 2 * u.kpc * kAtomBytes, kAtomBytes, u.kpc * kAtomBytes);
+                mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, kk ? 1u : 0u);
+              }
               mma_commit(&sm.tfull_ex[acc]);
             }
             __syncwarp();
           }
           if (lane == 0) {
             mma_commit(&sm.empty[st]);
+            if (kYReg) mbar_arrive_cnt(&sm.empty[st], 8);  // the epilogue never reads B-only stages
             if (s == u.nst - 1) mma_commit(&sm.vempty[vb]);
           }
           __syncwarp();
@@ -1059,6 +1132,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         if (r == 0 && p.trace) trace_put(p, k, 4, gtimer());
         tc_fence_after();
         ++nsh;
+        const bool split = p.mode == MODE_FUSED && u.ks > 1;
         for (int j = 0; j < u.jps; ++j) {
           const int job = u.job0 + j;
           for (int c0 = 0; c0 < u.rank; c0 += 32) {
@@ -1072,9 +1146,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
                 for (int i = 0; i < 32; ++i)
                   if (c0 + i < nv) dst[c0 + i] = v[i];
               }
+            } else if (split) {
+              // this K range's fp32 partial row (rows >= m are never read back)
+              if (r < u.m) {
+                float4* dst = reinterpret_cast<float4*>(part_of(p, job, u.tile) + ((size_t)u.kq * u.mp + r) * u.rp + c0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  if (c0 + i * 4 < u.rp) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              }
             } else if (r < u.mp) {
-              // this K range's partial V image (bf16); the expand MMAs accumulate the ks images
-              write_v_chunk(vimg_of(p, job, u.tile) + u.kq * u.vstride, u, r, c0, v, r < u.m ? u.rank : 0);
+              write_v_chunk(vimg_of(p, job, u.tile), u, r, c0, v, r < u.m ? u.rank : 0);  // the tile's V image
             }
           }
         }
@@ -1082,6 +1163,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty_sh[ab]);
         if (p.mode == MODE_SHRINK) continue;
+        if (split) {
+          // split-K arrival: the last of the tile's ks units of this job group sums the ks fp32
+          // partials in K order (deterministic) and writes the ONE bf16 V image
+          named_bar_sync(BAR_EPI + es, 128);
+          if (r == 0) {
+            __threadfence();  // release: this set's partial stores before the arrival
+            const int old = atomicAdd(p.arrive + u.tile * kMaxJobs + u.job0 / u.jps, 1);
+            __threadfence();  // acquire: the other units' partials after the arrival
+            sm.last_arr[es] = old == u.ks - 1;
+          }
+          named_bar_sync(BAR_EPI + es, 128);
+          if (!sm.last_arr[es]) continue;
+          for (int j = 0; j < u.jps; ++j) {
+            const int job = u.job0 + j;
+            const float* base = part_of(p, job, u.tile);
+            if (r < u.mp)
+              for (int c0 = 0; c0 < u.rank; c0 += 32) {
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                if (r < u.m)
+                  for (int kq = 0; kq < u.ks; ++kq) {
+                    const float4* src = reinterpret_cast<const float4*>(base + ((size_t)kq * u.mp + r) * u.rp + c0);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                      if (c0 + i * 4 < u.rp) {
+                        const float4 q = __ldcg(src + i);
+                        v[4 * i] += q.x; v[4 * i + 1] += q.y; v[4 * i + 2] += q.z; v[4 * i + 3] += q.w;
+                      }
+                  }
+                write_v_chunk(vimg_of(p, job, u.tile), u, r, c0, v, r < u.m ? u.rank : 0);
+              }
+          }
+        }
         post_event(p, sm, es, npost, u.tile, 2, r);
         continue;
       }
@@ -1091,6 +1206,61 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       const int yrow_idx = p.perm ? __ldg(p.perm + pos) : pos;
       const bool valid = r < u.m;
       char* const ybase_g = p.jobs[u.job].y;
+      if (kYReg) {
+        // Each thread owns tile row r (TMEM lane r): its 128-byte y piece of a 64-column group
+        // is loaded into registers one of its groups ahead (the loads overlap the B copies and
+        // the MMAs), D2 is added, and the row piece is stored back.  The ring carries B only.
+        seq += u.nst;
+        char* const yrow = ybase_g + (long long)yrow_idx * p.h_out * 2 + (long long)u.col0 * 2;
+        const int g0 = (es - (ngrp & 1)) & 1;  // this set's first group of the unit
+        uint4 ya[8], yb[8];
+        auto yload = [&](int g, uint4 (&buf)[8]) {
+          if (CHAM_EXP_NOEPI < 2 && valid && g < u.ngrp) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) buf[i] = __ldcs(reinterpret_cast<const uint4*>(yrow + g * 128) + i);
+          }
+        };
+        auto yupdate = [&](int g, uint4 (&buf)[8]) {
+          const int gi = ngrp + g;
+          const int acc = gi % NACC;
+          if (CHAM_EXP_NOEPI == 3) {  // experiment: the epilogue releases the accumulator unread
+            if (lane == 0) mbar_arrive(&sm.tempty_ex[acc]);
+            return;
+          }
+          pf_wait(p, &sm.tfull_ex[acc], (gi / NACC) & 1, 16, gi, u_id);
+          tc_fence_after();
+          float d0[32], d1[32];
+          tmem_ld32x2(tmem + TM_EX + acc * 64 + lane_off, d0, d1);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tempty_ex[acc]);
+          if (valid && !kNoEpi) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float* d = i < 4 ? d0 + i * 8 : d1 + (i - 4) * 8;
+              float f[8];
+              Elem<__nv_bfloat16>::unpack(buf[i], f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] += d[e];
+              __stcs(reinterpret_cast<uint4*>(yrow + g * 128) + i, Elem<__nv_bfloat16>::pack(f));
+            }
+          }
+        };
+        if (kYPrefetch && valid)  // this set's later groups of the unit: DRAM -> L2 now, registers later
+          for (int g = g0 + 2; g < u.ngrp; g += 2)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(yrow + g * 128) : "memory");
+        if (s_first_group_ok(g0, u.ngrp)) yload(g0, ya);
+        for (int g = g0; g < u.ngrp; g += 4) {
+          yload(g + 2, yb);
+          yupdate(g, ya);
+          if (g + 2 >= u.ngrp) break;
+          yload(g + 4, ya);
+          yupdate(g + 2, yb);
+        }
+        if (r == 0 && p.trace) trace_put(p, k, 4, gtimer());
+        ngrp += u.ngrp;
+        continue;
+      }
       for (int s = 0; s < u.nst; ++s, ++seq) {
         const int st = seq % NS;
         const int ng = min(u.kpc, u.ngrp - s * u.kpc);
@@ -1168,6 +1338,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   __syncthreads();
   if (sm.last[0]) {
     for (int i = tid; i < MAX_TILES; i += NTHREADS) p.tile_cnt[i] = 0;
+    for (int i = tid; i < MAX_TILES * kMaxJobs; i += NTHREADS) p.arrive[i] = 0;
     if (tid == 0) {
       p.ctr[0] = 0;
       p.ctr[1] = 0;
@@ -1268,6 +1439,8 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   int* pc = pool->d_pctr + (prm.epoch & 1) * (kPrefillCtrSet);
   prm.ctr = pc;
   prm.tile_cnt = pc + 4;
+  prm.arrive = pc + 4 + kPrefillMaxTiles;
+  prm.ppart = pool->d_ppart;
   prm.err = pool->d_ctr + 2;
   prm.vimg = pool->d_pvimg;
   prm.v_out = v_out;

@@ -280,8 +280,10 @@ def test_chained_launches_respect_pdl_dependencies(ntok):
     ref = [bufs[0]]
     for i in range(6):
         ref.append(bf16_round(lora_apply_ref(ref[i], bufs[i + 1], perm, seg_off, seg_slot, seg_rank, adapters)))
-    # a stale read would be O(1) wrong almost everywhere; bf16 rounding of the (prefill) V
-    # images compounds over the chain, so the tolerance is looser than a single apply's
+    # a stale read would be O(1) wrong almost everywhere.  The split-K shrink partials are
+    # summed in fp32 and the V image is rounded to bf16 once: rtol is the single apply's 2e-2,
+    # the absolute floor one bf16 ulp of the chain's largest outputs (|y| up to ~16: 0.0625),
+    # where an output rounded to the neighbouring bf16 value is not a numerical error
     for i in range(1, 7):
-        np.testing.assert_allclose(dev[i].float().cpu().numpy(), ref[i], rtol=3e-2, atol=1e-1)
+        np.testing.assert_allclose(dev[i].float().cpu().numpy(), ref[i], rtol=2e-2, atol=6.25e-2)
     pool.close()
