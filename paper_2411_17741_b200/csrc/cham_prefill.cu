@@ -70,9 +70,19 @@ constexpr int UQ = 8;                   // unit-id ring depth
 #define CHAM_PF_CD 1  // outstanding unit claims per loader (A/B on C3: 1 -> 590k, 4 -> 347k tok/s: early claims of expand units block on unready tiles)
 #endif
 constexpr int CD = CHAM_PF_CD;
+#ifndef CHAM_PF_EXSTATIC
+#define CHAM_PF_EXSTATIC 0  // 1: expand units assigned statically, round-robin (A/B on C3: 539k vs 634k tok/s dynamic)
+#endif
+constexpr bool kExStatic = CHAM_PF_EXSTATIC != 0;
 constexpr int MAX_TILES = kPrefillMaxTiles;
-constexpr int NTHREADS = 384;           // warps 0-7 epilogue (two sets of 4), 8 loader, 9 MMA, 10-11 publishers
-constexpr int W_LOAD = 8, W_MMA = 9, W_PUB = 10;
+constexpr int NTHREADS = 384;           // warps 0-7 epilogue (two sets of 4), 8-9 publishers, 10 MMA, 11 loader
+// The loader is the highest-numbered warp (the warp schedulers favour higher warp ids, so the
+// serial dispatch + copy-issue chain is not starved by the ALU-heavy epilogue warps).
+#ifndef CHAM_PF_LOADER_HI
+#define CHAM_PF_LOADER_HI 1  // 0: the round-1 numbering (loader 8, MMA 9, publishers 10-11)
+#endif
+constexpr int W_LOAD = CHAM_PF_LOADER_HI ? 11 : 8, W_MMA = CHAM_PF_LOADER_HI ? 10 : 9,
+              W_PUB = CHAM_PF_LOADER_HI ? 8 : 10;
 constexpr int PQN = 8;                  // publish ring depth per epilogue set
 constexpr int TMEM_COLS = 512;
 // TMEM: two shrink accumulators of TM_SH columns, then NACC expand accumulators of 64 columns
@@ -781,9 +791,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     // first unit static, the rest from the counter: lanes 0 .. CD-1 each hold one outstanding
     // claim (consumed round-robin and refilled at once), so a unit's id never waits for the
     // atomic's round trip
+    //   (CHAM_PF_EXSTATIC=1 assigns the expand units statically, CTA c taking u1 + c, u1 + c + G,
+    //   ...: no atomic on the loader's path, but it lost the A/B — tiles become ready unevenly.)
     int next = blockIdx.x;
     int claim = 1 << 29, chead = 0;
-    if (lane < CD && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
+    bool dyn = true;
+    int ex_j = 0;
+    if (kExStatic && next >= tl.u1) {
+      dyn = false;
+      next = tl.u1 + blockIdx.x;
+      ex_j = 1;
+    }
+    if (dyn && lane < CD && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
     // published phase-1 units of an expand unit's tile, read without blocking one unit ahead
     const int ex_per_tile = p.n_jobs * ((p.h_out + CW - 1) / CW);
     auto peek_flag = [&](int u) {  // unconditional (clamped) load: the value is used one unit later
@@ -816,10 +835,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       auto advance = [&]() {
         // the lanes' claims were issued together, so their order is not the counter's; an
         // exhausted claim (>= the unit count) is skipped until every lane's is
-        for (;;) {
+        if (kExStatic && !dyn) {
+          next = tl.u1 + blockIdx.x + ex_j * gridDim.x;
+          ++ex_j;
+        } else for (;;) {
           const int h = chead;
           chead = chead + 1 == CD ? 0 : chead + 1;
           next = __shfl_sync(0xffffffffu, claim, h) + gridDim.x;
+          if (kExStatic && next >= tl.u1) {  // phase-1 units exhausted: the static expand list
+            dyn = false;
+            next = tl.u1 + blockIdx.x;
+            ex_j = 1;
+            break;
+          }
           if (next < tl.u_total) {
             if (lane == h) claim = atomicAdd(p.ctr, 1);
             break;
@@ -919,11 +947,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         __syncwarp();
         ++nex;
         const int nblk = (u.m + 31) / 32;
-        bool contig[4];
-        int rows[4];
+        bool contig[4] = {false, false, false, false};
+        int rows[4] = {0, 0, 0, 0};
+        bool c64[2] = {false, false};
+        if (!kYReg) {  // the staged-y path's TMA boxes (the register path loads y in the epilogue)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(cf, u, b, lane, contig[b]) : 0;
-        const bool c64[2] = {block64(contig, rows, nblk, 0), nblk > 2 && block64(contig, rows, nblk, 1)};
+          for (int b = 0; b < 4; ++b) rows[b] = b < nblk ? block_row(cf, u, b, lane, contig[b]) : 0;
+          c64[0] = block64(contig, rows, nblk, 0);
+          c64[1] = nblk > 2 && block64(contig, rows, nblk, 1);
+        }
         const bool pad = (u.rp / 8) > u.np;
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
@@ -979,7 +1011,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       }
       if (kWarmL2 && next < tl.u_total) warm_l2(p, make_unit(p, tl, next), pf, lane);
     }
-  } else if (warp >= W_PUB) {
+  } else if (warp == W_PUB || warp == W_PUB + 1) {
     publisher(p, sm, warp - W_PUB);
   } else if (warp == W_MMA) {
     // ---------------------------------------------------------------- MMA issuer
