@@ -5,27 +5,30 @@
 // performs that work for real, y[t] += (x[t] . A_slot) . B_slot, for every segment with at
 // least `prefill_min_tokens` tokens (rank <= 128, bf16).
 //
-// ONE persistent, warp-specialised kernel per lora_apply (K3).  A tile is up to
-// 128 token rows of one segment (UMMA M = 128).  Units are dispatched dynamically from one
-// counter, phase-1 units first:
-//   shrink unit (tile, K-split kq, job group): D[128 x rp] (TMEM, fp32) = X . A^T over the
-//        unit's h_in range, for every job of the group from ONE x stage (q/k/v share x, so x
-//        crosses HBM->SM once per K range).  Stages carry kpc 64-column k-chunks: x by TMA
-//        tensor loads of exactly the tile's rows (32-row boxes, or 1-row boxes when the rows
-//        are not contiguous), A^T page atoms by 1 KiB bulk copies straight from the pool
-//        layout (K-major SWIZZLE_128B already).  The epilogue writes fp32 partial v rows; the
-//        last unit of a tile (split-K arrival counter) sums them and writes the tile's V image
-//        (bf16, K-major SWIZZLE_128B, exactly the UMMA A-operand layout) and publishes it
-//        (tile flag = launch epoch).
-//   expand unit (tile, job, 512 columns): the loader waits for the tile's V flag, copies the V
-//        image (one bulk copy), then streams 64-column groups: B page slices (MN-major
-//        SWIZZLE_128B — the pool layout again) + the y rows of the group.  D2[128 x 64] =
-//        V . B per group (double-buffered TMEM); the epilogue adds D2 to the y rows and stores
-//        them — no separate elementwise kernel.
-// Expand units wait only for their own tile, so the phases overlap.  Warps 0-3: epilogue (TMEM
-// lanes 0-127, one token row per thread); warp 4: loader (TMA + dispatch); warp 5: MMA issuer.
-// The path is HBM-bound (AI ~15 flop/B at C3): tensor cores are used because the CUDA-core
-// FMA ceiling (~51-74 TFLOP/s) is below what the HBM roofline demands.
+// ONE persistent, warp-specialised kernel per lora_apply (K3), one CTA per SM, 12
+// warps: 0-7 epilogue (two sets of four, each set covering the 128 TMEM lanes), 8-9 publishers
+// (one per epilogue set), 10 MMA issuer, 11 loader (TMA + dispatch; the highest warp id, so
+// the schedulers favour it).  A tile is up to 128 token rows of one segment (UMMA M = 128).
+// Units come from one dynamic counter, phase-1 units first:
+//   shrink unit (tile, K range kq of ks, job group): D[128 x rp] (TMEM, fp32) = X . A^T over the
+//        range, for every job of the group from ONE x stage (q/k/v share x, so x crosses
+//        HBM->SM once per K range).  Stages carry kpc 64-column k-chunks: x by TMA tensor loads
+//        of exactly the tile's rows (64-row boxes, or 1-row boxes when the rows are not
+//        consecutive tokens), A^T page atoms by bulk copies straight from the pool layout
+//        (K-major SWIZZLE_128B already).  With ks > 1 the epilogue writes the range's fp32
+//        partial; the last of the ks arrivals (per tile and job group) sums the partials in K
+//        order — deterministic, one bf16 rounding — into the tile's V image (bf16, K-major
+//        SWIZZLE_128B: exactly the UMMA A-operand layout); with ks = 1 the image is written
+//        directly.  The publisher releases the image (tile counter += 1).
+//   expand unit (tile, job, CW = 256 columns): the loader waits for the tile's images, copies
+//        the V image (one bulk copy, double-buffered), then streams the B page slices of the
+//        unit's 64-column groups (MN-major SWIZZLE_128B — the pool layout again).  D2[128 x 64]
+//        = V . B per group into one of four TMEM accumulators; the epilogue thread of token
+//        row r loads its 128-byte y piece of the group into registers one group ahead, adds
+//        D2 and stores it back — no separate elementwise kernel, no y in shared memory.
+// Expand units wait only for their own tile, so the phases overlap across tiles.  The path is
+// HBM-bound (AI ~15 flop/B at C3): tensor cores are used because the CUDA-core FMA ceiling
+// (~51-74 TFLOP/s) is below what the HBM roofline demands.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
