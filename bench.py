@@ -456,6 +456,27 @@ def measure(config: str, args, rank: int, world: int, e2e: bool = True) -> dict:
     return out
 
 
+def sub_record(config: str, args, rank: int, world: int) -> dict:
+    """C4 (cache with misses) / C5 (70B dims, TP = world) measured in the same driver run as the
+    C2 line, with short step counts; a failure is recorded, never fatal to the headline line."""
+    import copy
+
+    import torch
+
+    a = copy.copy(args)
+    a.steps, a.warmup = (20, 3) if config == "c4" else (10, 3)
+    try:
+        line = (run_c4 if config == "c4" else run_c5)(a, rank, world, emit=False)
+    except Exception as e:  # pragma: no cover - reported in the line
+        torch.cuda.synchronize()
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    finally:
+        torch.cuda.empty_cache()
+    keep = ("value", "unit", "ms_per_step", "steps", "warmup", "config", "roofline", "cache", "decisions",
+            "adapter_read_gbs_per_rank", "gpu_launches", "clocks", "device_error")
+    return {k: line[k] for k in keep if k in line}
+
+
 def roofline_record(m: dict, config: str) -> dict:
     hbm_peak, bf16_peak, peak_kind = peaks()
     achieved = m["bytes_step"] / (m["apply_ms"] * 1e-3) / 1e9
@@ -523,6 +544,11 @@ def run_ours(args, rank: int, world: int):
             "clocks": c3["clocks"], "device_error": c3["device_error"],
             "gpu_launches": args.steps * c3["launches_per_step"]}
         line["gpu_launches"] += line["c3"]["gpu_launches"]
+    if args.config == "c2" and world == 1 and not args.no_subrecords:
+        line["c4"] = sub_record("c4", args, rank, world)
+        line["c5"] = sub_record("c5", args, rank, world)
+        for k in ("c4", "c5"):
+            line["gpu_launches"] += line[k].get("gpu_launches", 0) if isinstance(line[k], dict) else 0
     if world == 1 and not args.no_cpu_baseline:
         from bench_decisions import cpu_model
 
@@ -537,7 +563,7 @@ def run_ours(args, rank: int, world: int):
 
 
 # --------------------------------------------------------------------------- C4: cache with misses
-def run_c4(args, rank: int, world: int):
+def run_c4(args, rank: int, world: int, emit: bool = True):
     """C4 replica: 1000-adapter Zipf(0.7) catalog, PagedAdapterCache at 10% of idle HBM, a
     closed loop of 256 decode requests (each step's zipf draws, seeded by replica rank and
     step, replace the requests the previous step executed), admitted up to 256 per step.  A step is `serving.ReplicaLoop.step`: fill completions by
@@ -677,8 +703,12 @@ def run_c4(args, rank: int, world: int):
             "gpu_launches": state["batches"] * ex.launches_per_step(),
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
+        pool.close()
+        return line
     pool.close()
+    return None
 
 
 def enum_name(v):
@@ -693,7 +723,7 @@ H70_OUT = [8192, 1024, 1024, 8192]  # GQA: 8 KV heads
 C5_ADAPTERS, C5_RANK = 100, 64
 
 
-def run_c5(args, rank: int, world: int):
+def run_c5(args, rank: int, world: int, emit: bool = True):
     """C5: Llama-2-70B dims (80 layers; q/o 8192->8192, k/v 8192->1024), 100 adapters of rank 64,
     decode batch of 256 tokens, tensor parallel over the N ranks (TP = N; every rank sees the
     same tokens).  A step = per layer: shrink of the rank's x shard for q/k/v into one fused
@@ -820,8 +850,12 @@ def run_c5(args, rank: int, world: int):
             "gpu_launches": args.steps * L70 * (5 if world > 1 else 3),
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
+        pool.close()
+        return line
     pool.close()
+    return None
 
 
 def main():
@@ -839,6 +873,7 @@ def main():
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (tcgen05 prefill) sub-record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefetch", action="store_true", help="C4: prefetch off (the reference's default)")
+    ap.add_argument("--no-subrecords", action="store_true", help="C2 line without the C4/C5 sub-records")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
