@@ -10,6 +10,8 @@
 #include <cstring>
 #include <string>
 
+#include <vector>
+
 #include "cham_pool.h"
 
 namespace cham {
@@ -171,6 +173,7 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     cudaFree(pool->d_pvimg);
     cudaFree(pool->d_ppart);
     cudaFree(pool->d_pctr);
+    cudaFree(pool->d_iota);
     cudaFree(pool->d_split);
     cudaFree(pool->d_split_ctr);
     delete pool;
@@ -213,6 +216,12 @@ int cham_pool_create(cham_pool** out, int device, int n_pages, int n_layers, int
     e = cudaMalloc(&pool->d_ppart, (size_t)kMaxJobs * kPrefillMaxTiles * kPrefillPart);
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMalloc(&pool->d_pctr, sizeof(int) * prefill_ctr_ints());
   if (e == cudaSuccess && pool->prefill_ok) e = cudaMemset(pool->d_pctr, 0, sizeof(int) * prefill_ctr_ints());
+  if (e == cudaSuccess && pool->prefill_ok) e = cudaMalloc(&pool->d_iota, sizeof(int) * (size_t)max_tokens);
+  if (e == cudaSuccess && pool->prefill_ok) {
+    std::vector<int> iota(max_tokens);
+    for (int i = 0; i < max_tokens; ++i) iota[i] = i;
+    e = cudaMemcpy(pool->d_iota, iota.data(), sizeof(int) * (size_t)max_tokens, cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) return cleanup(CHAM_ERR_OOM, "cham_pool_create: workspace allocation failed");
   cudaMemset(pool->d_slot_pages, 0xff, sizeof(int) * (size_t)n_slots * kMaxPagesPerSlot);
   cudaMemset(pool->d_slot_rank, 0, sizeof(int) * (size_t)n_slots);
@@ -236,6 +245,7 @@ int cham_pool_destroy(cham_pool* pool) {
   cudaFree(pool->d_pvimg);
   cudaFree(pool->d_ppart);
   cudaFree(pool->d_pctr);
+  cudaFree(pool->d_iota);
   cudaFree(pool->d_split);
   cudaFree(pool->d_split_ctr);
   delete pool;

@@ -40,6 +40,7 @@ struct cham_pool {
   int route_max_seg = 1 << 30;
   char* d_pvimg = nullptr;             // prefill V images [kMaxJobs][kPrefillMaxTiles][32 KiB] (bf16, one per tile)
   float* d_ppart = nullptr;            // prefill split-K fp32 partials [kMaxJobs][kPrefillMaxTiles][64 KiB]
+  int* d_iota = nullptr;               // identity token rows [max_tokens] (prefill calls without perm)
   int* d_pctr = nullptr;               // prefill counters: 2 parity sets + tile V flags
   int prefill_epoch = 0;               // prefill launches so far (tile flags, counter parity)
   float* d_split = nullptr;            // decode page-half partials [kMaxJobs][kSplitCap][split_ncc][4][2048 B cols]
@@ -61,7 +62,7 @@ constexpr int kPrefillMaxSplit = 8;    // shrink split-K factor bound (workspace
 constexpr int kPrefillMaxTiles = 256;  // 128-row prefill tiles per apply (workspace sizing)
 constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles + kPrefillMaxTiles * cham::kMaxJobs;  // one parity set:
 // dispatch, done, spare x2, tile V counters [tiles], split-K arrival counters [tiles][groups]
-constexpr size_t kPrefillPart = 65536;                 // fp32 split-K partial bytes per (job, tile)
+constexpr size_t kPrefillPart = 262144;                // fp32 split-K partial bytes per (job, tile): 8 K ranges at rank 128
 constexpr size_t kPrefillVImg = 32768;                // V image bytes per (job, tile)
 inline size_t prefill_ctr_ints() { return 2 * kPrefillCtrSet + kPrefillMaxTiles; }
 

@@ -69,6 +69,9 @@ constexpr bool kYPrefetch = CHAM_PF_YPF != 0;
 constexpr int CW = CHAM_PF_CW;          // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
+#ifndef CHAM_PF_KS_WAVES
+#define CHAM_PF_KS_WAVES 2  // shrink K-split: grow until the phase-1 units fill this many waves
+#endif
 #ifndef CHAM_PF_CD
 #define CHAM_PF_CD 1  // outstanding unit claims per loader (A/B on C3: 1 -> 590k, 4 -> 347k tok/s: early claims of expand units block on unready tiles)
 #endif
@@ -109,7 +112,7 @@ struct Job {
 // Activation tensor maps of one job: a 64-column x 64-row box for contiguous rows and a
 // 64-column x 1-row box for gathered ones, both SWIZZLE_128B (x for shrink, y for expand).
 struct alignas(64) Maps {
-  CUtensorMap x64, x1, y64, y1;
+  CUtensorMap x64, x1, y64, y1, y32;  // y32: 32-row boxes of the standalone expand kernel
 };
 
 struct alignas(64) Params {
@@ -121,6 +124,7 @@ struct alignas(64) Params {
   int h_in, h_out;
   int n_jobs;
   int mode;
+  int no_expand;           // MODE_FUSED without expand units: V images only (expand_kernel follows)
   int x_shared;            // every job reads the same x (q/k/v): one x stage serves the group
   const int* perm;
   const int* seg_off;
@@ -375,7 +379,8 @@ struct TileList {
   int ks;           // shrink K-split factor
   int u1;           // phase-1 units
   int u_total;
-  int sh_start[MAX_TILES + 1];
+  int sh_start[MAX_TILES + 1];  // phase-1 unit prefix over the LPT order
+  int ord[MAX_TILES];            // LPT order of the phase-1 units: position -> tile (rank descending)
   Tile t[MAX_TILES];
 };
 
@@ -436,13 +441,29 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
   for (int o = 16; o >= 1; o >>= 1) groups += __shfl_xor_sync(0xffffffffu, groups, o);
   int ks = 1;
   if (p.mode == MODE_FUSED)
-    while (ks < kPrefillMaxSplit && groups * ks < 2 * grid && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8) ks *= 2;
-  // phase-1 unit prefix (vbuild units in MODE_EXPAND: one per tile)
+    while (ks < kPrefillMaxSplit && groups * ks < CHAM_PF_KS_WAVES * grid && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8)
+      ks *= 2;
+  // LPT order of the phase-1 units: tiles by padded rank, descending (stable) — the long
+  // K loops of the large-rank tiles start first instead of forming the launch's tail
+  {
+    int pos = 0;
+    for (int b = MAXR / 16; b >= 1; --b)
+      for (int base = 0; base < tiles; base += 32) {
+        const int t = base + lane;
+        const bool f = t < tiles && rpad(tl.t[t].rank) / 16 == b;
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) tl.ord[pos + __popc(m & ((1u << lane) - 1))] = t;
+        pos += __popc(m);
+      }
+    __syncwarp();
+  }
+  // phase-1 unit prefix over the LPT order (vbuild units in MODE_EXPAND: one per tile)
   int carry = 0;
   for (int base = 0; base < tiles; base += 32) {
-    const int t = base + lane;
+    const int k = base + lane;
     int u = 0;
-    if (t < tiles) {
+    if (k < tiles) {
+      const int t = tl.ord[k];
       int kt = ks;
       const int part = mpad(tl.t[t].m) * rpad(tl.t[t].rank) * 4;  // one K range's fp32 partial
       while (kt > 1 && kt * part > (int)kPrefillPart) kt >>= 1;
@@ -455,7 +476,7 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
       const int a = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += a;
     }
-    if (t < tiles) tl.sh_start[t] = carry + inc - u;
+    if (k < tiles) tl.sh_start[k] = carry + inc - u;
     carry += __shfl_sync(0xffffffffu, inc, 31);
   }
   if (lane == 0) {
@@ -464,7 +485,7 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
     tl.sh_start[tiles] = carry;
     tl.u1 = carry;
     const int ncc = (p.h_out + CW - 1) / CW;
-    tl.u_total = carry + (p.mode == MODE_SHRINK ? 0 : tiles * p.n_jobs * ncc);
+    tl.u_total = carry + ((p.mode == MODE_SHRINK || p.no_expand) ? 0 : tiles * p.n_jobs * ncc);
   }
   return true;
 }
@@ -495,8 +516,10 @@ struct Unit {
 
 __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, int u) {
   Unit x;
+  int k = 0;  // LPT position of a phase-1 unit's tile
   if (u < tl.u1) {
-    x.tile = tile_of_unit(tl, u);
+    k = tile_of_unit(tl, u);
+    x.tile = tl.ord[k];
     x.kind = p.mode == MODE_EXPAND ? 3 : 1;
   } else {
     const int ncc = (p.h_out + CW - 1) / CW;
@@ -520,7 +543,7 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
   x.ks = t.ks;
   x.vstride = ((x.rp + 63) / 64) * x.xb;
   if (x.kind == 1) {
-    const int rem = u - tl.sh_start[x.tile];
+    const int rem = u - tl.sh_start[k];
     x.kq = rem % t.ks;
     x.jps = jobs_per_group(p, t.rank);
     x.job0 = (rem / t.ks) * x.jps;
@@ -559,13 +582,13 @@ __device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileLis
   }
   const bool ok = u_id >= 0 && u_id < tl.u_total;
   const int uu = ok ? u_id : 0;
-  const int ti = uu < tl.u1 ? tile_of_unit(tl, uu) : (uu - tl.u1) / (p.n_jobs * ((p.h_out + CW - 1) / CW));
+  const int ti = uu < tl.u1 ? tl.ord[tile_of_unit(tl, uu)] : (uu - tl.u1) / (p.n_jobs * ((p.h_out + CW - 1) / CW));
   const Tile& t = tl.t[ti];
   f.page = __ldg(p.slot_pages + t.slot * kMaxPagesPerSlot + min(lane, kMaxPagesPerSlot - 1));
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
     const int pos = t.pos0 + min(b * 32 + lane, t.m - 1);
-    f.rows[b] = p.perm ? __ldg(p.perm + pos) : pos;
+    f.rows[b] = __ldg(p.perm + pos);  // perm is never null (identity rows from the pool)
   }
   return f;
 }
@@ -860,9 +883,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         }
         if (lane == 0) trace_ld(p, k, 1);
         flag = peek_flag(next);
+        if (lane == 0) trace_ld(p, k, 6);
         pf = prefetch_unit(p, tl, next, lane);
       };
       advance();
+      if (lane == 0) trace_ld(p, k, 7);
       const Unit u = make_unit(p, tl, u_id);
       if (lane == 0 && p.trace) {
         trace_put(p, k, 0, gtimer());
@@ -1238,7 +1263,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       // ---- expand: y rows += D2 per 64-column group.  Each thread adds its row in place in
       // the staged y tile; then the warp stores its 32 rows coalesced (8 lanes per 128-byte
       // row, 4 rows per instruction) instead of 32 rows x 16 B per instruction.
-      const int yrow_idx = p.perm ? __ldg(p.perm + pos) : pos;
+      const int yrow_idx = __ldg(p.perm + pos);
       const bool valid = r < u.m;
       char* const ybase_g = p.jobs[u.job].y;
       if (kYReg) {
@@ -1383,6 +1408,552 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   crumb(p, 5, gtimer());
 }
 
+
+// =========================================================================== expand kernel
+// The standalone expand phase of a prefill apply (CHAM_PF_SPLITX): the fused kernel runs in
+// shrink-only mode (no_expand: it publishes the tiles' V images and stops), then this kernel
+// streams y += V . B with no dependency left inside the launch — every V image is final once
+// griddepcontrol.wait returns — so the work is split statically: each CTA owns one contiguous
+// range of items (tile, job, column block), balanced by bytes, and runs it as a plain pipeline
+// without claims, readiness polls or per-unit global round trips on the loader's path.
+//   warp 0 loader: per item one ring stage = the y rows of the item's G 64-column groups
+//          (TMA, 32-row SWIZZLE_128B boxes, 1-row boxes for non-consecutive rows) + the B page
+//          slices of those groups (bulk copies straight from the page layout, [page][group]
+//          atoms: the MN-major SWIZZLE_128B B operand); per run of items of one (tile, job)
+//          the V image (double-buffered).
+//   warp 1 MMA: D[128 x 64] = V . B per group into one of eight TMEM accumulators.
+//   warps 2-5 epilogue: thread = tile row = TMEM lane; adds D to its y row piece IN the stage
+//          (swizzled 16-byte chunks: conflict-free), then the warp TMA-stores its 32 rows back
+//          (one box when they are 32 consecutive valid tokens, else one row box per row).
+// Arithmetic is the fused kernel's: the same V image, the same UMMA sequence, y + D rounded
+// once to bf16 — the two paths give bit-identical y.
+#ifndef CHAM_PF_SPLITX
+#define CHAM_PF_SPLITX 0  // 1: fused-mode applies run as shrink-only fused kernel + expand_kernel (A/B on C3: 540k vs 630k tok/s fused)
+#endif
+#ifndef CHAM_PFX_NS
+#define CHAM_PFX_NS 6
+#endif
+constexpr int XNS = CHAM_PFX_NS;     // ring stages
+constexpr int XSTAGE = 24576;        // bytes per stage (y of G groups of <= 64 rows + their B slices)
+constexpr int XACC = 8;              // TMEM accumulators of 64 fp32 columns (all 512 columns)
+#ifndef CHAM_PFX_SETS
+#define CHAM_PFX_SETS 2              // epilogue sets (4 warps each) working on alternate items
+#endif
+constexpr int XSETS = CHAM_PFX_SETS;
+constexpr int X_THREADS = 64 + 128 * XSETS;  // warp 0 loader, 1 MMA, then the epilogue sets
+constexpr int XROWS = 64;            // rows of an expand item (a half of a 128-row tile)
+constexpr int XYB = XROWS * 128;     // y bytes of one 64-column group of an item
+constexpr int XVB = 2 * XYB;         // V buffer: the item rows of <= 2 K-blocks (rank <= 128)
+#ifndef CHAM_PFX_IDY
+#define CHAM_PFX_IDY 1  // y added on the tensor cores: D = I . Y + V . B (epilogue: convert + store only)
+#endif
+constexpr bool kIdY = CHAM_PFX_IDY != 0;
+#ifndef CHAM_PFX_EXP
+#define CHAM_PFX_EXP 0  // experiment builds: 1 the epilogue skips the y add, 2 waits for each item's stores
+#endif
+#ifndef CHAM_PFX_LAG
+#define CHAM_PFX_LAG 1               // items (of one set) whose y stores may still read their stage
+#endif
+constexpr int XLAG = CHAM_PFX_LAG;
+static_assert(XACC * 64 <= TMEM_COLS, "TMEM budget");
+static_assert(XNS > XSETS * (XLAG + 1), "ring depth");
+
+struct XShared {
+  alignas(1024) unsigned char stage[XNS][XSTAGE];
+  // two V buffers + one pad: the UMMA A operand spans 128 rows, the image has 64 per K-block
+  alignas(1024) unsigned char vbuf[2 * XVB + XYB];
+  // kIdY: A operand [128 rows x 64 K] = the identity on rows < 64 (K-major SWIZZLE_128B)
+  alignas(1024) unsigned char ident[kIdY ? BM * 128 : 16];
+  uint64_t full[XNS], empty[XNS];
+  uint64_t tfull[XACC], tempty[XACC];
+  uint64_t vfull[2], vempty[2];
+  uint64_t drain;
+  uint32_t tmem_base;
+  int ok;
+  int lo, hi;            // this CTA's items [lo, hi)
+  int t0, h0, j0, cb0;   // (tile, half, job, column block) of item lo
+  TileList tl;
+};
+static_assert(sizeof(XShared) <= 227 * 1024, "expand kernel shared memory exceeds 227 KiB");
+
+// Per-tile item geometry: G 64-column groups per item, as many as one stage holds.
+struct XGeom {
+  int rp, np, npad;  // ranks (16-padded), pages, pages incl. the zero pad
+  int nh;            // 64-row halves of the tile
+  int G, ncb;        // groups per item, items per (tile, half, job)
+  int xb;            // K-block stride of the tile's V image (mp rows x 128 B)
+};
+__device__ __forceinline__ XGeom xgeom(const Params& p, const Tile& t) {
+  XGeom g;
+  g.rp = rpad(t.rank);
+  g.np = (t.rank + 7) / 8;
+  g.npad = g.rp / 8;
+  g.nh = (t.m + XROWS - 1) / XROWS;
+  g.xb = mpad(t.m) * 128;
+  g.G = max(1, min(8, XSTAGE / (XYB + g.npad * kAtomBytes)));
+  const int ngr = p.h_out / 64;
+  g.ncb = (ngr + g.G - 1) / g.G;
+  return g;
+}
+// Byte weight of one item of tile t (y read + written, B read): the balance unit.
+__device__ __forceinline__ long long xweight(const Tile& t, const XGeom& g) {
+  return (long long)g.G * (2LL * min(t.m, XROWS) * 128 + (long long)g.np * kAtomBytes);
+}
+
+// Warp 0: this CTA's item range, by byte weight (items in (tile, half, job, block) order).
+__device__ void x_range(const Params& p, XShared& sm) {
+  const int lane = threadIdx.x & 31;
+  const TileList& tl = sm.tl;
+  const int n = tl.n_tiles;
+  const int K = (n + 31) / 32;  // tiles per lane, contiguous
+  const int ta = min(n, lane * K), tb = min(n, ta + K);
+  long long w = 0;
+  int items = 0;
+  for (int t = ta; t < tb; ++t) {
+    const XGeom g = xgeom(p, tl.t[t]);
+    const int it = g.nh * p.n_jobs * g.ncb;
+    items += it;
+    w += it * xweight(tl.t[t], g);
+  }
+  long long wpre = w;
+  int ipre = items;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long a = __shfl_up_sync(0xffffffffu, wpre, o);
+    const int b = __shfl_up_sync(0xffffffffu, ipre, o);
+    if (lane >= o) {
+      wpre += a;
+      ipre += b;
+    }
+  }
+  const long long W = __shfl_sync(0xffffffffu, wpre, 31);
+  const int NI = __shfl_sync(0xffffffffu, ipre, 31);
+  wpre -= w;  // exclusive
+  ipre -= items;
+  // the first item whose start weight is >= S, and its (tile, half, job, block)
+  auto locate = [&](long long S, int (&res)[5]) {
+    const bool mine = S >= wpre && S < wpre + w;
+    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+    int r[5] = {NI, n, 0, 0, 0};
+    if (mine && lane == __ffs(bal) - 1) {
+      long long acc = wpre;
+      int ib = ipre;
+      for (int t = ta; t < tb; ++t) {
+        const XGeom g = xgeom(p, tl.t[t]);
+        const long long wi = xweight(tl.t[t], g);
+        const int it = g.nh * p.n_jobs * g.ncb;
+        if (S < acc + it * wi) {
+          const int k = (int)((S - acc + wi - 1) / wi);
+          if (k >= it) {
+            r[0] = ib + it;
+            r[1] = t + 1;
+          } else {
+            r[0] = ib + k;
+            r[1] = t;
+            r[2] = k / (p.n_jobs * g.ncb);
+            r[3] = (k / g.ncb) % p.n_jobs;
+            r[4] = k % g.ncb;
+          }
+          break;
+        }
+        acc += it * wi;
+        ib += it;
+      }
+    }
+    const int src = bal ? __ffs(bal) - 1 : 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int v = __shfl_sync(0xffffffffu, r[i], src);
+      res[i] = bal ? v : (i == 0 ? NI : i == 1 ? n : 0);
+    }
+  };
+  const long long S0 = W * (long long)blockIdx.x / gridDim.x;
+  const long long S1 = W * (long long)(blockIdx.x + 1) / gridDim.x;
+  int r0[5], r1[5];
+  locate(S0, r0);
+  int hi = NI;
+  if (blockIdx.x + 1 != gridDim.x) {
+    locate(S1, r1);
+    hi = r1[0];
+  }
+  if (lane == 0) {
+    sm.lo = r0[0];
+    sm.hi = max(r0[0], hi);
+    sm.t0 = r0[1];
+    sm.h0 = r0[2];
+    sm.j0 = r0[3];
+    sm.cb0 = r0[4];
+  }
+}
+
+// Item cursor: (tile, half, job, column block) in item order.
+struct XCursor {
+  int t, h, j, cb;
+  __device__ __forceinline__ void next(int n_jobs, const XGeom& g) {
+    if (++cb == g.ncb) {
+      cb = 0;
+      if (++j == n_jobs) {
+        j = 0;
+        if (++h == g.nh) {
+          h = 0;
+          ++t;
+        }
+      }
+    }
+  }
+};
+
+// debug timeline (trace builds): the first half of the debug buffer, units 64 + i: item i of
+// the CTA's range: 0 loader issued, 1 MMA got the stage, 2 epilogue got it, 3 epilogue done;
+// unit 63: lo, hi, start time
+__device__ __forceinline__ void xtrace(const Params& p, int i, int field, unsigned long long v) {
+  const int k = 64 + i;
+  if (p.trace && k < p.trace_cap)
+    p.trace[(((long long)blockIdx.x - (long long)gridDim.x) * p.trace_cap + k) * 8 + field] = v;
+}
+
+__global__ void __launch_bounds__(X_THREADS, 1) expand_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  XShared& sm = *reinterpret_cast<XShared*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < XNS; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1 + 128);  // MMA commit + every epilogue thread (its stores read)
+    }
+    for (int i = 0; i < XACC; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.vfull[i], 1);
+      mbar_init(&sm.vempty[i], 1);
+    }
+    mbar_init(&sm.drain, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane < p.n_jobs) {
+    prefetch_map(&p.maps[lane].y32);
+    prefetch_map(&p.maps[lane].y1);
+  }
+  if (kIdY) {
+    for (int i = tid; i < BM * 8; i += X_THREADS) {  // row i / 8, 16-byte chunk i % 8 (K cols 8c..8c+7)
+      const int rr = i >> 3, ch = i & 7;
+      uint32_t w[4] = {0, 0, 0, 0};
+      if (rr < XROWS && (rr >> 3) == ch) w[(rr & 7) >> 1] = (rr & 1) ? 0x3F800000u : 0x00003F80u;
+      *reinterpret_cast<uint4*>(sm.ident + swz(rr, ch)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    fence_proxy_async_shared();  // generic stores -> the UMMA's async-proxy reads
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm.tmem_base);
+    tc_fence_before();
+  }
+  if (warp == 0) {
+    const bool ok = build_tiles(p, sm.tl, gridDim.x);
+    if (lane == 0) sm.ok = ok ? 1 : 0;
+    if (ok) x_range(p, sm);
+  }
+  __syncthreads();
+  tc_fence_after();
+  const TileList& tl = sm.tl;
+  const uint32_t tmem = sm.tmem_base;
+  const int lo = sm.ok ? sm.lo : 0, hi = sm.ok ? sm.hi : 0;
+  if (!sm.ok && tid == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
+  if (tid == 0) {
+    xtrace(p, -1, 0, lo);
+    xtrace(p, -1, 1, hi);
+    xtrace(p, -1, 2, gtimer());
+  }
+  const int ngr = p.h_out / 64;
+  if (warp == 0) {
+    // ---------------------------------------------------------------- loader
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_y = policy_evict_first();
+    XCursor c{sm.t0, sm.h0, sm.j0, sm.cb0};
+    int cur_t = -1, cur_h = -1, cur_j = -1, nrun = -1, seq = 0, mh = 0;
+    int rows[2] = {0, 0}, rf[2] = {0, 0};  // this lane's row / the 32-row block's first row
+    bool c32[2] = {false, false};
+    int page = 0;
+    XGeom g{};
+    bool waited = false;
+    for (int it = lo; it < hi; ++it, c.next(p.n_jobs, g)) {
+      const Tile& T = tl.t[c.t];
+      if (c.t != cur_t) {
+        g = xgeom(p, T);
+        page = __ldg(p.slot_pages + T.slot * kMaxPagesPerSlot + min(lane, kMaxPagesPerSlot - 1));
+      }
+      if (c.t != cur_t || c.h != cur_h) {
+        mh = min(XROWS, T.m - c.h * XROWS);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          rows[b] = __ldg(p.perm + T.pos0 + c.h * XROWS + min(b * 32 + lane, mh - 1));
+          rf[b] = __shfl_sync(0xffffffffu, rows[b], 0);
+          c32[b] = __all_sync(0xffffffffu, b * 32 + lane >= mh || rows[b] == rf[b] + lane);
+        }
+      }
+      if (!waited) {  // V images (the shrink kernel) and y (earlier applies) come from earlier grids
+        pdl_wait();
+        pdl_launch_dependents();
+        waited = true;
+      }
+      if (c.t != cur_t || c.h != cur_h || c.j != cur_j) {
+        ++nrun;
+        const int vb = nrun & 1;
+        const int nkb = (g.rp + 63) / 64;
+        if (lane == 0) {
+          if (nrun >= 2) mbar_wait(&sm.vempty[vb], ((nrun >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(&sm.vfull[vb], nkb * XYB);
+        }
+        __syncwarp();
+        // the half's 64 rows of each K-block of the tile's V image
+        if (lane < nkb)
+          bulk_g2s(sm.vbuf + vb * XVB + lane * XYB, vimg_of(p, c.j, c.t) + lane * g.xb + c.h * XYB, XYB,
+                   &sm.vfull[vb], pol_w);
+        cur_t = c.t;
+        cur_h = c.h;
+        cur_j = c.j;
+      }
+      const int s = seq % XNS;
+      if (lane == 0 && seq >= XNS) mbar_wait(&sm.empty[s], ((seq / XNS) - 1) & 1);
+      __syncwarp();
+      unsigned char* st = sm.stage[s];
+      unsigned char* bst = st + g.G * XYB;  // B atoms [page][group], page stride G KiB
+      const int col0 = c.cb * g.G * 64;
+      const int ng = min(g.G, ngr - c.cb * g.G);
+      if (g.npad > g.np) {
+        // zero atoms for the K rows rank..rp (V is zero there; 0 x stale NaN would not be)
+        uint4* z = reinterpret_cast<uint4*>(bst + g.np * g.G * kAtomBytes);
+        for (int i = lane; i < (g.npad - g.np) * g.G * (kAtomBytes / 16); i += 32) z[i] = make_uint4(0, 0, 0, 0);
+        fence_proxy_async_shared();
+      }
+      __syncwarp();
+      // both 32-row blocks consecutive: one 64-row box per group
+      const bool c64 = mh > 32 && c32[0] && c32[1] && rf[1] == rf[0] + 32;
+      uint32_t ybytes = 0;
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+        if (b * 32 < mh) ybytes += c32[b] ? 32 * 128 : min(32, mh - b * 32) * 128;
+      if (CHAM_PFX_EXP == 4) ybytes = 0;
+      if (kIdY && (mh < XROWS || !c32[0] || !c32[1])) {
+        // the identity MMA reads all 64 y rows of a group: rows no box covers must be finite
+        for (int gi = 0; gi < ng; ++gi)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            if (c32[b] && b * 32 < mh) continue;  // the box fills all 32 rows
+            for (int i = lane; i < 32 * 8; i += 32) {
+              const int rr = b * 32 + (i >> 3);
+              if (rr >= mh) *reinterpret_cast<uint4*>(st + gi * XYB + rr * 128 + (i & 7) * 16) = make_uint4(0, 0, 0, 0);
+            }
+          }
+        fence_proxy_async_shared();
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive_expect_tx(&sm.full[s], ng * (g.np * kAtomBytes + ybytes));
+      __syncwarp();
+      if (lane < g.np)
+        bulk_g2s(bst + lane * g.G * kAtomBytes,
+                 p.base + (long long)page * p.page_bytes + p.jobs[c.j].b_off + (long long)(col0 / 64) * kAtomBytes,
+                 ng * kAtomBytes, &sm.full[s], pol_w);
+      for (int gi = 0; gi < (CHAM_PFX_EXP == 4 ? 0 : ng); ++gi) {
+        unsigned char* yd = st + gi * XYB;
+        if (c64 && CHAM_PFX_EXP == 3) {
+          if (lane == 0) tma_load_2d(yd, &p.maps[c.j].y64, col0 + gi * 64, rf[0], &sm.full[s], pol_y);
+          continue;
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          if (b * 32 >= mh) continue;
+          if (c32[b]) {
+            if (lane == 0) tma_load_2d(yd + b * 32 * 128, &p.maps[c.j].y32, col0 + gi * 64, rf[b], &sm.full[s], pol_y);
+          } else if (b * 32 + lane < mh) {
+            tma_load_2d(yd + (b * 32 + lane) * 128, &p.maps[c.j].y1, col0 + gi * 64, rows[b], &sm.full[s], pol_y);
+          }
+        }
+      }
+      if (lane == 0) xtrace(p, it - lo, 0, gtimer());
+      ++seq;
+    }
+    if (!waited) {
+      pdl_wait();
+      pdl_launch_dependents();
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = idesc_bf16(BM, 64, true);
+    XCursor c{sm.t0, sm.h0, sm.j0, sm.cb0};
+    int cur_t = -1, cur_h = -1, cur_j = -1, nrun = -1, seq = 0, nacc = 0;
+    XGeom g{};
+    for (int it = lo; it < hi; ++it) {
+      if (c.t != cur_t) g = xgeom(p, tl.t[c.t]);
+      if (c.t != cur_t || c.h != cur_h || c.j != cur_j) {
+        ++nrun;
+        mbar_wait(&sm.vfull[nrun & 1], (nrun >> 1) & 1);
+        cur_t = c.t;
+        cur_h = c.h;
+        cur_j = c.j;
+      }
+      const int s = seq % XNS;
+      mbar_wait(&sm.full[s], (seq / XNS) & 1);
+      if (lane == 0) xtrace(p, it - lo, 1, gtimer());
+      tc_fence_after();
+      const uint32_t va = smem_u32(sm.vbuf + (nrun & 1) * XVB);
+      const uint32_t bb = smem_u32(sm.stage[s] + g.G * XYB);
+      const int ng = min(g.G, ngr - c.cb * g.G);
+      for (int gi = 0; gi < ng; ++gi, ++nacc) {
+        const int a = nacc % XACC;
+        if (nacc >= XACC) mbar_wait(&sm.tempty[a], ((nacc / XACC) - 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          if (kIdY) {  // D = I . Y: the group's y rows (MN-major SWIZZLE_128B B operand, K = rows)
+            const uint32_t ia = smem_u32(sm.ident), yb = smem_u32(sm.stage[s] + gi * XYB);
+            for (int kk = 0; kk < XROWS / 16; ++kk)
+              mma_bf16(tmem + a * 64, sdesc(ia + kk * 32, 16, 1024), sdesc(yb + kk * 2 * kAtomBytes, kAtomBytes, kAtomBytes),
+                       idesc, kk ? 1u : 0u);
+          }
+          for (int kk = 0; kk < g.rp / 16; ++kk) {
+            const uint64_t ad = sdesc(va + (kk >> 2) * XYB + (kk & 3) * 32, 16, 1024);
+            const uint64_t bd = sdesc(bb + gi * kAtomBytes + kk * 2 * g.G * kAtomBytes, kAtomBytes, g.G * kAtomBytes);
+            mma_bf16(tmem + a * 64, ad, bd, idesc, (kIdY || kk) ? 1u : 0u);
+          }
+          mma_commit(&sm.tfull[a]);
+        }
+        __syncwarp();
+      }
+      const int vb = nrun & 1;
+      XCursor nx = c;
+      nx.next(p.n_jobs, g);
+      const bool run_end = it + 1 == hi || nx.t != c.t || nx.h != c.h || nx.j != c.j;
+      if (lane == 0) {
+        mma_commit(&sm.empty[s]);
+        if (run_end) mma_commit(&sm.vempty[vb]);
+      }
+      __syncwarp();
+      c = nx;
+      ++seq;
+    }
+    // drain: the commit arrivals above are asynchronous and must land before the CTA exits
+    if (lane == 0) mma_commit(&sm.drain);
+    __syncwarp();
+    mbar_wait(&sm.drain, 0);
+  } else {
+    // ---------------------------------------------------------------- epilogue sets
+    // set es (warps 2 + 4 es .. 5 + 4 es, one per TMEM lane quarter) takes the items with
+    // (item - lo) % XSETS == es; every set walks the whole item stream for the cursors
+    const int es = (warp - 2) >> 2;
+    const int eq = warp & 3;                 // TMEM lane quarter of this warp
+    const int r = eq * 32 + lane;            // item row (rows >= 64 are the UMMA's padding)
+    const uint32_t lane_off = (uint32_t)(eq * 32) << 16;
+    XCursor c{sm.t0, sm.h0, sm.j0, sm.cb0};
+    int cur_t = -1, cur_h = -1, seq = 0, nacc = 0;
+    int pend[XLAG + 1];                      // stages whose stores may still read them
+#pragma unroll
+    for (int i = 0; i <= XLAG; ++i) pend[i] = -1;
+    int row = 0, row0 = 0, mh_cur = 0;
+    bool box = false, valid = false;
+    XGeom g{};
+    for (int it = lo; it < hi; ++it) {
+      const Tile& T = tl.t[c.t];
+      if (c.t != cur_t) g = xgeom(p, T);
+      if ((it - lo) % XSETS != es) {  // another set's item
+        nacc += min(g.G, ngr - c.cb * g.G);
+        c.next(p.n_jobs, g);
+        ++seq;
+        continue;
+      }
+      if (c.t != cur_t || c.h != cur_h) {
+        const int mh = min(XROWS, T.m - c.h * XROWS);
+        mh_cur = mh;
+        valid = r < mh;
+        row = __ldg(p.perm + T.pos0 + c.h * XROWS + min(r, mh - 1));
+        row0 = __shfl_sync(0xffffffffu, row, 0);
+        // one 32-row box store when the warp's rows are 32 consecutive valid tokens
+        box = __all_sync(0xffffffffu, valid && row == row0 + lane);
+        cur_t = c.t;
+        cur_h = c.h;
+      }
+      const int s = seq % XNS;
+      mbar_wait(&sm.full[s], (seq / XNS) & 1);
+      if (eq == 0 && lane == 0) xtrace(p, it - lo, 2, gtimer());
+      unsigned char* st = sm.stage[s];
+      const int col0 = c.cb * g.G * 64;
+      const int ng = min(g.G, ngr - c.cb * g.G);
+      for (int gi = 0; gi < ng; ++gi, ++nacc) {
+        const int a = nacc % XACC;
+        mbar_wait(&sm.tfull[a], (nacc / XACC) & 1);
+        tc_fence_after();
+        float d0[32], d1[32];
+        const bool wvalid = eq * 32 < mh_cur;  // warp-uniform: this quarter holds item rows
+        if (!kIdY || wvalid) tmem_ld32x2(tmem + a * 64 + lane_off, d0, d1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty[a]);
+        if (kIdY) {
+          if (valid) {  // D = y + V . B in fp32: round once, back into the stage for the TMA store
+            unsigned char* yr = st + gi * XYB;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const float* d = ch < 4 ? d0 + ch * 8 : d1 + (ch - 4) * 8;
+              float f[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] = d[e];
+              *reinterpret_cast<uint4*>(yr + swz(r, ch)) = Elem<__nv_bfloat16>::pack(f);
+            }
+          }
+          continue;
+        }
+        if (eq == 0 && lane == 0 && gi == 0) xtrace(p, it - lo, 7, gtimer());  // group 0's accumulator in registers
+        if (valid && CHAM_PFX_EXP != 1) {
+          unsigned char* yr = st + gi * XYB;
+          uint4 yv[8];  // all eight 16-byte chunks of the row piece in flight at once
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) yv[ch] = *reinterpret_cast<const uint4*>(yr + swz(r, ch));
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            float f[8];
+            Elem<__nv_bfloat16>::unpack(yv[ch], f);
+            const float* d = ch < 4 ? d0 + ch * 8 : d1 + (ch - 4) * 8;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] += d[e];
+            *reinterpret_cast<uint4*>(yr + swz(r, ch)) = Elem<__nv_bfloat16>::pack(f);
+          }
+        }
+      }
+      if (eq == 0 && lane == 0) xtrace(p, it - lo, 4, gtimer());
+      // the generic-proxy y writes -> the TMA stores (async proxy) of this warp's rows
+      fence_proxy_async_shared();
+      __syncwarp();
+      if (eq == 0 && lane == 0) xtrace(p, it - lo, 5, gtimer());
+      if (box) {
+        if (lane == 0)
+          for (int gi = 0; gi < ng; ++gi)
+            tma_store_2d(&p.maps[c.j].y32, col0 + gi * 64, row0, st + gi * XYB + eq * 32 * 128);
+      } else if (valid) {
+        for (int gi = 0; gi < ng; ++gi)
+          tma_store_2d(&p.maps[c.j].y1, col0 + gi * 64, row, st + gi * XYB + r * 128);
+      }
+      bulk_commit();
+      if (eq == 0 && lane == 0) xtrace(p, it - lo, 6, gtimer());
+      if (CHAM_PFX_EXP == 2) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      // the stores of the item XLAG back have read their stage: release it
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(XLAG) : "memory");
+#pragma unroll
+      for (int i = XLAG; i > 0; --i) pend[i] = pend[i - 1];
+      pend[0] = s;
+      if (pend[XLAG] >= 0) mbar_arrive(&sm.empty[pend[XLAG]]);
+      if (eq == 0 && lane == 0) xtrace(p, it - lo, 3, gtimer());
+      c.next(p.n_jobs, g);
+      ++seq;
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every y store performed
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem);
+  }
+}
+
 }  // namespace prefill
 
 namespace {
@@ -1440,8 +2011,11 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   static bool attr_set = false;
   if (!attr_set) {
     CHAM_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Shared)));
+    CHAM_CUDA(cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(XShared)));
     attr_set = true;
   }
+  // fused mode as two launches: shrink-only fused kernel (V images), then expand_kernel
+  const bool splitx = mode == MODE_FUSED && CHAM_PF_SPLITX;
   if (mode != MODE_FUSED && n_jobs != 1) return fail(CHAM_ERR_INVALID, "prefill shrink/expand take one projection");
   Params prm{};
   prm.base = pool->base;
@@ -1463,7 +2037,9 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
     prm.jobs[j].a_off = (long long)pool->a_off[lp];
     prm.jobs[j].b_off = (long long)pool->b_off[lp];
   }
-  prm.perm = perm;
+  // an unconditional row load: `perm ? perm[pos] : pos` would compile to a load merged with a
+  // select that waits for the load where it is issued (one L2 round trip per loader unit)
+  prm.perm = perm ? perm : pool->d_iota;
   prm.seg_off = seg_off;
   prm.seg_slot = seg_slot;
   prm.seg_rank = seg_rank;
@@ -1494,6 +2070,7 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
     if (!rc && mode != MODE_SHRINK) {
       rc = encode_act_map(&prm.maps[j].y64, ys[j], n_tokens, prm.h_out, 64);
       if (!rc) rc = encode_act_map(&prm.maps[j].y1, ys[j], n_tokens, prm.h_out, 1);
+      if (!rc && splitx) rc = encode_act_map(&prm.maps[j].y32, ys[j], n_tokens, prm.h_out, 32);
     }
     if (rc) return rc;
   }
@@ -1507,7 +2084,13 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CHAM_PF_PDL ? 1 : 0;
+  prm.no_expand = splitx ? 1 : 0;
   CHAM_CUDA(cudaLaunchKernelEx(&cfg, fused_kernel, prm));
+  if (splitx) {
+    cfg.blockDim = dim3(X_THREADS);
+    cfg.dynamicSmemBytes = sizeof(XShared);
+    CHAM_CUDA(cudaLaunchKernelEx(&cfg, expand_kernel, prm));
+  }
   return CHAM_OK;
 }
 
