@@ -62,7 +62,7 @@ constexpr int kPrefillMaxSplit = 8;    // shrink split-K factor bound (workspace
 constexpr int kPrefillMaxTiles = 256;  // 128-row prefill tiles per apply (workspace sizing)
 constexpr int kPrefillCtrSet = 4 + kPrefillMaxTiles + kPrefillMaxTiles * cham::kMaxJobs;  // one parity set:
 // dispatch, done, spare x2, tile V counters [tiles], split-K arrival counters [tiles][groups]
-constexpr size_t kPrefillPart = 262144;                // fp32 split-K partial bytes per (job, tile): 8 K ranges at rank 128
+constexpr size_t kPrefillPart = 131072;                // fp32 split-K partial bytes per (job, tile): 2 K ranges at 128 rows x rank 128
 constexpr size_t kPrefillVImg = 32768;                // V image bytes per (job, tile)
 inline size_t prefill_ctr_ints() { return 2 * kPrefillCtrSet + kPrefillMaxTiles; }
 

@@ -40,14 +40,14 @@ namespace prefill {
 constexpr int BM = 128;                 // tokens per tile (UMMA M)
 constexpr int MAXR = kPrefillMaxRank;   // rank rows per adapter on this path
 #ifndef CHAM_PF_NS
-#define CHAM_PF_NS 4
+#define CHAM_PF_NS 2  // ring stages x bytes: A/B on C3 (tok/s): 4 x 32K 630k, 3 x 32K 651k, 2 x 64K 656k, 2 x 48K 677k
 #endif
 #ifndef CHAM_PF_VBUF
 #define CHAM_PF_VBUF (2 * 128 * 128)
 #endif
 constexpr int NS = CHAM_PF_NS;          // ring stages
 #ifndef CHAM_PF_STAGE
-#define CHAM_PF_STAGE 32768
+#define CHAM_PF_STAGE 49152  // two big stages: shrink stages carry 2-3 K-chunks (A copies of 2-3 KiB, not 1 KiB)
 #endif
 constexpr int STAGE = CHAM_PF_STAGE;    // bytes per ring stage
 constexpr int VPAD = BM * 128 - 4096;   // worst over-read past a V buffer: 16 KiB - the smallest x block
@@ -69,6 +69,9 @@ constexpr bool kYPrefetch = CHAM_PF_YPF != 0;
 constexpr int CW = CHAM_PF_CW;          // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
+#ifndef CHAM_PF_KS_MAX
+#define CHAM_PF_KS_MAX 2  // largest shrink K-split; A/B on C3 with 2 x 48K stages: 8 677k, 2 744k, 1 663k tok/s
+#endif
 #ifndef CHAM_PF_KS_WAVES
 #define CHAM_PF_KS_WAVES 2  // shrink K-split: grow until the phase-1 units fill this many waves
 #endif
@@ -441,7 +444,7 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
   for (int o = 16; o >= 1; o >>= 1) groups += __shfl_xor_sync(0xffffffffu, groups, o);
   int ks = 1;
   if (p.mode == MODE_FUSED)
-    while (ks < kPrefillMaxSplit && groups * ks < CHAM_PF_KS_WAVES * grid && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8)
+    while (ks < CHAM_PF_KS_MAX && groups * ks < CHAM_PF_KS_WAVES * grid && nkc % (2 * ks) == 0 && nkc / (2 * ks) >= 8)
       ks *= 2;
   // LPT order of the phase-1 units: tiles by padded rank, descending (stable) — the long
   // K loops of the large-rank tiles start first instead of forming the launch's tail
