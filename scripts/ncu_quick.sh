@@ -14,5 +14,5 @@ for r in rows:
 for (i, k), m in by.items():
     us = float(m["gpu__time_duration.sum"]) / 1e3
     rd = float(m["dram__bytes_read.sum"]) / 1e6; wr = float(m["dram__bytes_write.sum"]) / 1e6
-    print(f"{i:>3} {k:28s} {us:8.1f} us  read {rd:7.1f} MB  write {wr:6.1f} MB  {(rd + wr) / us / 1e3:5.2f} TB/s  warps {m['sm__warps_active.avg.pct_of_peak_sustained_active']}")
+    print(f"{i:>3} {k:28s} {us:8.1f} us  read {rd:7.1f} MB  write {wr:6.1f} MB  {(rd + wr) / us:5.2f} TB/s  warps {m['sm__warps_active.avg.pct_of_peak_sustained_active']}")
 PY
