@@ -109,7 +109,7 @@ constexpr int K2_STAGE = K2_V + 8 * TG * kRowsPerPage * 4;  // v slice [page][to
 // per unit of the tier-0 geometry, whose 1-page stages were consumer- and issue-bound
 // (0.9 us per 25 KB stage on C2).  Stage layout: B [8 rows][4096 B] | y [TG][4096 B] | v [TG][8].
 #ifndef CHAM_WIDE_NP
-#define CHAM_WIDE_NP 4
+#define CHAM_WIDE_NP 4  // A/B (tok/s, page-ready tiles, release publication): C2 4 -> 131.2k, 8 -> 132.0k, 16 -> 115.3k; C5 4 -> 24.25k, 8 -> 23.5k
 #endif
 constexpr int kWideNp = CHAM_WIDE_NP;
 constexpr int TIER_W = 3;
@@ -1194,11 +1194,11 @@ __device__ __forceinline__ UnitPos locate(const Params& p, const Plan& pl, const
 }
 
 #ifndef CHAM_PUB_FENCE
-#define CHAM_PUB_FENCE 1  // publisher: fence + relaxed atomic (1) or one release reduction (0)
+#define CHAM_PUB_FENCE 0  // publisher: fence + relaxed atomic (1) or one release reduction / release OR (0); A/B on C2 with page-ready tiles: 131.5k vs 132.8k (wide 8)
 #endif
 constexpr bool kPubFence = CHAM_PUB_FENCE != 0;
 #ifndef CHAM_PAGE_READY
-#define CHAM_PAGE_READY 0  // 1: tile counters as page bitmasks, an expand stage waits for its own pages only (C2 117.0k vs 117.3k)
+#define CHAM_PAGE_READY 1  // 1: tile counters as page bitmasks, an expand stage waits for its own pages only (round 1: C2 117.0k vs 117.3k; round 2: 131.0k vs 130.3k)
 #endif
 constexpr bool kPageReady = CHAM_PAGE_READY != 0;
 // pages [pg0, pg0 + n) of a tile as a mask (np <= 32 pages per adapter)
@@ -1627,9 +1627,12 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
         mbar_arrive(&sm.pub_empty[slot]);
         if (!c) break;
         if (kPubFence) __threadfence();  // explicit fence before the release (A/B switch)
-        if (kPageReady && bits)
-          atomicOr(reinterpret_cast<unsigned*>(c), bits);  // page g of the tile is final
-        else if (kPubFence)
+        if (kPageReady && bits) {  // page g of the tile is final
+          if (kPubFence)
+            atomicOr(reinterpret_cast<unsigned*>(c), bits);
+          else
+            red_release_gpu_or(reinterpret_cast<unsigned*>(c), bits);  // release, cumulative as below
+        } else if (kPubFence)
           atomicAdd(c, 1);  // tile counters without page masks; split-unit partials
         else
           red_release_gpu_add(c, 1);  // release is cumulative over the consumers' v stores
