@@ -163,6 +163,13 @@ struct Params {
   int n_seg;
   const int* n_seg_dev;
   int* ctr;        // [0] next shrink unit, [1] finished CTAs, [4] next expand unit
+  // CHAM_ZERO_NEXT: the other parity's counter set (the previous apply's), re-armed by this
+  // apply's producers right after griddepcontrol.wait, before launch_dependents
+  int* zero_ctr;
+  int* zero_tile;
+  long long zero_tile_n;
+  int* zero_split;
+  long long zero_split_n;
   int* tile_ctr;   // MODE_FUSED: [job][expand tile] shrink units finished (v rows published)
   float* split_buf;   // page-half partials [job][split tile][col chunk][TG][cols of a chunk]
   int* split_ctr;     // [job][split tile][col chunk]: half 0 published its partial
@@ -320,6 +327,31 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Counter re-arming (CHAM_ZERO_NEXT).  Apply n counts in parity set n % 2.  Once its
+// griddepcontrol.wait returned, apply n-1 (the other set's user) is complete, so producer 0 of
+// every CTA zeroes its slice of the other set and only then signals launch_dependents: apply
+// n+1 cannot start before every slice is zero, and no CTA of apply n needs a last-CTA reset
+// (an L2 atomic and a fence on every CTA's exit path) any more.
+#ifndef CHAM_ZERO_NEXT
+#define CHAM_ZERO_NEXT 1
+#endif
+constexpr bool kZeroNext = CHAM_ZERO_NEXT != 0;
+__device__ __forceinline__ void after_wait(const Params& p, int pid) {
+  if (!kZeroNext) {
+    pdl_launch_dependents();
+    return;
+  }
+  if (pid != 0) return;  // producer 0 signals, after the re-arm
+  const int lane = threadIdx.x & 31;
+  const long long step = (long long)gridDim.x * 32;
+  for (long long i = (long long)blockIdx.x * 32 + lane; i < p.zero_tile_n; i += step) p.zero_tile[i] = 0;
+  for (long long i = (long long)blockIdx.x * 32 + lane; i < p.zero_split_n; i += step) p.zero_split[i] = 0;
+  if (blockIdx.x == 0 && lane < 16) p.zero_ctr[lane] = 0;
+  __threadfence();
+  __syncwarp();
+  pdl_launch_dependents();
 }
 
 // Reduce-scatter of NV (power of two <= 32) per-lane partial sums across a warp: returns
@@ -1237,10 +1269,10 @@ __device__ __forceinline__ void pend_add(PendingX& q, const char* src, void* dst
 }
 // wait for the previous kernel (x, y and the workspaces may be its outputs), then issue the
 // held-back x copies
-__device__ __forceinline__ void pend_flush(PendingX& q, bool& waited, uint64_t pol_x) {
+__device__ __forceinline__ void pend_flush(const Params& p, int pid, PendingX& q, bool& waited, uint64_t pol_x) {
   if (waited) return;
   pdl_wait();
-  pdl_launch_dependents();
+  after_wait(p, pid);
   waited = true;
 #pragma unroll
   for (int i = 0; i < NSTAGE; ++i)
@@ -1276,7 +1308,7 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
     const uint32_t x_bytes = a_bytes / kRowsPerPage;
     unsigned char* st = sm.stage[stage];
     // a stage's second use waits for consumers that need their x rows: release them first
-    if (seq >= NSTAGE) pend_flush(pend, waited, pol_x);
+    if (seq >= NSTAGE) pend_flush(p, pid, pend, waited, pol_x);
     if (lane == 0) mbar_wait(&sm.empty[stage], ((seq / NSTAGE) & 1) ^ 1);
     const unsigned long long t_ready = p.trace ? gtimer() : 0;
     __syncwarp();
@@ -1301,7 +1333,7 @@ __device__ __forceinline__ int issue_shrink(const Params& p, Shared& sm, int seq
     if (!waited && CHAM_EARLY_A) {  // x may be produced by the previous kernel: hold it back
       pend_add(pend, x_src, st + A_CHUNK + lane * X_PITCH, &sm.full[stage], x_bytes, lane < tcount);
     } else {
-      pend_flush(pend, waited, pol_x);
+      pend_flush(p, pid, pend, waited, pol_x);
       if (lane < tcount) bulk_g2s(st + A_CHUNK + lane * X_PITCH, x_src, x_bytes, &sm.full[stage], pol_x);
     }
     if (lane == 0) trace_producer(p, seq, t_it, t_ready, 1, a_bytes + x_bytes * tcount);
@@ -1315,7 +1347,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
                                             bool fused, int job, int cc, int tile, int half, int tier, int4 da,
                                             int4 db, int rdy, int unit, int pid) {
   constexpr int ES = Elem<T>::kBytes;
-  pend_flush(pend, waited, policy_evict_last());
+  pend_flush(p, pid, pend, waited, policy_evict_last());
   const Plan& pl = sm.plan;
   const int lane = threadIdx.x & 31;
   const int NTL = pl.totals[1];
@@ -1420,7 +1452,7 @@ __device__ __forceinline__ int issue_expand(const Params& p, Shared& sm, int seq
     }
     if (!waited) {  // y may be produced by the previous kernel
       pdl_wait();
-      pdl_launch_dependents();
+      after_wait(p, pid);
       waited = true;
     }
     if (y_here && lane < tcount)
@@ -1565,7 +1597,7 @@ __device__ __forceinline__ int produce_all(const Params& p, Shared& sm, int seq,
     f0 = f1;
     f1 = f2;
   }
-  pend_flush(pend, waited, policy_evict_last());
+  pend_flush(p, pid, pend, waited, policy_evict_last());
   return seq;
 }
 
@@ -1644,7 +1676,10 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
     bool waited = false;
     int seq = 0;
     seq = produce_all<T>(p, sm, seq, waited, mode, pid);
-    if (!waited) pdl_wait();
+    if (!waited) {
+      pdl_wait();
+      after_wait(p, pid);  // a CTA without units still re-arms its slice
+    }
     if (lane == 0 && (NPROD == 1 || (seq & 1) == pid)) post_marker(sm, seq, KIND_END);
     if (pid == 0 && p.nx_items > 0) prefetch_next_apply(p, sm.plan, lane);
   } else {
@@ -1704,6 +1739,10 @@ __global__ void __launch_bounds__(APPLY_THREADS, 1) lora_apply_kernel(const __gr
   }
   // the last CTA re-arms the unit counters and the tile counters for the next launch
   if (tid == 0) trace_cta(p, 3);
+  if (kZeroNext) {  // the next apply re-arms this parity's counters (after_wait)
+    if (tid == 0) trace_cta(p, 4);
+    return;
+  }
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -1774,6 +1813,14 @@ int launch(cham_pool* pool, Params& prm, int mode, cudaStream_t stream) {
   prm.split_ncc = pool->split_ncc;
   prm.split_ctr = pool->d_split_ctr + (pool->apply_count & 1) * (size_t)kMaxJobs * kSplitCap * pool->split_ncc;
   prm.err = pool->d_ctr + 2;
+  {
+    const int o = (pool->apply_count + 1) & 1;  // the other parity: the previous apply's set
+    prm.zero_ctr = pool->d_ctr + 16 + o * 16;
+    prm.zero_tile = pool->d_ctr + kTileCtrBase + o * (size_t)kMaxJobs * pool->max_tokens;
+    prm.zero_tile_n = (long long)kMaxJobs * pool->max_tokens;
+    prm.zero_split = pool->d_split_ctr + o * (size_t)kMaxJobs * kSplitCap * pool->split_ncc;
+    prm.zero_split_n = (long long)kMaxJobs * kSplitCap * pool->split_ncc;
+  }
   ++pool->apply_count;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pool->sm_count);
