@@ -69,6 +69,10 @@ constexpr bool kYPrefetch = CHAM_PF_YPF != 0;
 constexpr int CW = CHAM_PF_CW;          // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 constexpr int UQ = 8;                   // unit-id ring depth
+#ifndef CHAM_PF_ZERO_NEXT
+#define CHAM_PF_ZERO_NEXT 1  // counters re-armed by the next launch after its griddepcontrol.wait
+#endif
+constexpr bool kPfZeroNext = CHAM_PF_ZERO_NEXT != 0;
 #ifndef CHAM_PF_KS_MAX
 #define CHAM_PF_KS_MAX 2  // largest shrink K-split; A/B on C3 with 2 x 48K stages: 8 677k, 2 744k, 1 663k tok/s
 #endif
@@ -142,6 +146,8 @@ struct alignas(64) Params {
   int* arrive;             // this parity's split-K arrival counters [MAX_TILES][kMaxJobs] (tile, job group)
   float* ppart;            // fp32 split-K partials [job][tile][kPrefillPart / 4]
   int* err;
+  int* zero_set;           // CHAM_PF_ZERO_NEXT: the other parity's counter set (the previous launch's)
+  int zero_n;
   char* vimg;              // V images [job][tile][VBUF]
   float* v_out;            // MODE_SHRINK: v [position][v_stride]
   const float* v_in;       // MODE_EXPAND: v [position][v_stride]
@@ -809,6 +815,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   pdl_wait();  // x, y, v and the workspaces may belong to the previous kernel
   if (CHAM_PF_PROXYFENCE) fence_proxy_async_global();
   crumb(p, 2, gtimer());
+  if (kPfZeroNext) {
+    // the previous launch (the other parity's user) is complete: re-arm its counter set, a
+    // slice per CTA, before this launch lets the next one start (no last-CTA reset at exit)
+    for (int i = blockIdx.x * NTHREADS + tid; i < p.zero_n; i += gridDim.x * NTHREADS) p.zero_set[i] = 0;
+    __threadfence();
+    __syncthreads();
+  }
   pdl_launch_dependents();
   if (!sm.flag) {
     if (tid == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
@@ -1393,6 +1406,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   if (warp == W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem);
+  }
+  if (kPfZeroNext) {  // the next launch re-arms this parity's counters
+    crumb(p, 5, gtimer());
+    return;
   }
   if (tid == 0) {
     __threadfence();
@@ -2051,6 +2068,8 @@ int prefill_launch(cham_pool* pool, int layer, int n_jobs, const int* projs, con
   prm.thr = prefill_route_thr(pool);
   prm.epoch = ++pool->prefill_epoch;
   int* pc = pool->d_pctr + (prm.epoch & 1) * (kPrefillCtrSet);
+  prm.zero_set = pool->d_pctr + ((prm.epoch + 1) & 1) * (kPrefillCtrSet);
+  prm.zero_n = kPrefillCtrSet;
   prm.ctr = pc;
   prm.tile_cnt = pc + 4;
   prm.arrive = pc + 4 + kPrefillMaxTiles;
