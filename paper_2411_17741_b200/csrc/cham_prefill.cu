@@ -46,8 +46,14 @@ constexpr int MAXR = kPrefillMaxRank;   // rank rows per adapter on this path
 #define CHAM_PF_VBUF (2 * 128 * 128)
 #endif
 constexpr int NS = CHAM_PF_NS;          // ring stages
+#ifndef CHAM_PF_LD2
+#define CHAM_PF_LD2 0  // 1: two loader warps in the expand phase (alternate unit positions; the second publisher warp loads); A/B on C3: 709k vs 763k — the epilogue (y RMW, ~1.7 us per group per set) then limits, and the 64 KiB stages it needs cost 3%
+#endif
+constexpr bool kLd2 = CHAM_PF_LD2 != 0;
 #ifndef CHAM_PF_STAGE
-#define CHAM_PF_STAGE 49152  // two big stages: shrink stages carry 2-3 K-chunks (A copies of 2-3 KiB, not 1 KiB)
+// two big stages: shrink stages carry 2-3 K-chunks (A copies of 2-3 KiB, not 1 KiB); with two
+// loaders every expand unit must fit one stage (4 groups x 16 KiB of B at rank 128)
+#define CHAM_PF_STAGE (CHAM_PF_LD2 ? 65536 : 49152)
 #endif
 constexpr int STAGE = CHAM_PF_STAGE;    // bytes per ring stage
 constexpr int VPAD = BM * 128 - 4096;   // worst over-read past a V buffer: 16 KiB - the smallest x block
@@ -96,6 +102,8 @@ constexpr int NTHREADS = 384;           // warps 0-7 epilogue (two sets of 4), 8
 #endif
 constexpr int W_LOAD = CHAM_PF_LOADER_HI ? 11 : 8, W_MMA = CHAM_PF_LOADER_HI ? 10 : 9,
               W_PUB = CHAM_PF_LOADER_HI ? 8 : 10;
+constexpr int W_LOAD2 = W_PUB + 1;  // kLd2: the second loader (one publisher serves both sets)
+constexpr int kUnitLoaderDone = -2;  // kLd2: a loader ran out of units (its later positions are skipped)
 constexpr int PQN = 8;                  // publish ring depth per epilogue set
 constexpr int TMEM_COLS = 512;
 // TMEM: two shrink accumulators of TM_SH columns, then NACC expand accumulators of 64 columns
@@ -680,6 +688,8 @@ struct Shared {
   uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[NACC], tempty_ex[NACC];
   uint64_t vfull[2], vempty[2];
   uint64_t drain;  // the MMA warp's last commit: every earlier commit arrival has landed
+  uint64_t ho_bar;  // kLd2: loader 0 hands the odd expand positions to loader 1
+  int ho_k0, ho_seq0, ho_nex0, ho_ok;
   uint64_t ufull[UQ], uempty[UQ];
   int uslot[UQ];
   uint32_t tmem_base;
@@ -759,6 +769,37 @@ __device__ void publisher(const Params& p, Shared& sm, int es) {
   }
 }
 
+// One publisher warp for both epilogue sets (CHAM_PF_LD2: the other warp loads): the two
+// queues are probed without blocking, each in its own order.
+__device__ void publisher_both(const Params& p, Shared& sm) {
+  const int lane = threadIdx.x & 31;
+  int k[2] = {0, 0};
+  bool done[2] = {false, false};
+  while (!done[0] || !done[1]) {
+    bool any = false;
+#pragma unroll
+    for (int es = 0; es < 2; ++es) {
+      if (done[es]) continue;
+      const int q = k[es] % PQN;
+      if (!mbar_test_wait(&sm.pq_full[es][q], (k[es] / PQN) & 1)) continue;
+      any = true;
+      const int tile = sm.pq_tile[es][q], kind = sm.pq_kind[es][q];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.pq_empty[es][q]);
+      ++k[es];
+      if (kind == 0) {
+        done[es] = true;
+        continue;
+      }
+      if (lane == 0) {
+        __threadfence();  // cumulative over the epilogue set's image stores
+        red_release_gpu_add(p.tile_cnt + tile, 1);
+      }
+    }
+    if (!any) __nanosleep(32);
+  }
+}
+
 // =========================================================================== the kernel
 __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -783,6 +824,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       mbar_init(&sm.tempty_ex[i], 4);
     }
     mbar_init(&sm.drain, 1);
+    mbar_init(&sm.ho_bar, 1);
     for (int i = 0; i < UQ; ++i) {
       mbar_init(&sm.ufull[i], 1);
       mbar_init(&sm.uempty[i], 1 + 8);
@@ -825,8 +867,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
   pdl_launch_dependents();
   if (!sm.flag) {
     if (tid == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
-  } else if (warp == W_LOAD) {
+  } else if (warp == W_LOAD || (kLd2 && warp == W_LOAD2)) {
     // ---------------------------------------------------------------- loader + dispatch
+    // kLd2: loader 0 runs the shrink phase alone; at its first expand unit (position k0) it
+    // hands positions k0 + 1, k0 + 3, ... to loader 1 and keeps k0, k0 + 2, ...  Every expand
+    // unit is one ring stage and one V buffer, so position parity owns one stage and one V
+    // buffer: each loader's waits stay in its own order.  A loader out of units posts
+    // kUnitLoaderDone; the consumers then skip its positions.
+    const int ld = (kLd2 && warp == W_LOAD2) ? 1 : 0;
     const uint64_t pol_w = policy_evict_first();  // adapter pages: streamed
     const uint64_t pol_x = CHAM_PF_XPOL_NORMAL == 1 ? policy_evict_normal() : CHAM_PF_XPOL_NORMAL == 2 ? policy_evict_first() : policy_evict_last();  // x: re-read by the other job groups / K ranges
     const uint64_t pol_y = policy_evict_first();
@@ -839,7 +887,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     int claim = 1 << 29, chead = 0;
     bool dyn = true;
     int ex_j = 0;
-    if (kExStatic && next >= tl.u1) {
+    bool two = false;                // two-loader positions (k0 + ld + 2i)
+    int h_k0 = 0, h_seq0 = 0, h_nex0 = 0;
+    bool idle = false;               // loader 1 without a handoff
+    if (ld == 1) {
+      mbar_wait(&sm.ho_bar, 0);
+      idle = !sm.ho_ok;
+      h_k0 = sm.ho_k0;
+      h_seq0 = sm.ho_seq0;
+      h_nex0 = sm.ho_nex0;
+      two = true;
+      int c0 = 1 << 29;
+      if (!idle && lane == 0) c0 = atomicAdd(p.ctr, 1);
+      next = __shfl_sync(0xffffffffu, c0, 0) + gridDim.x;
+    } else if (kExStatic && next >= tl.u1) {
       dyn = false;
       next = tl.u1 + blockIdx.x;
       ex_j = 1;
@@ -857,14 +918,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     Prefetch pf = prefetch_unit(p, tl, next, lane);
     if (kWarmL2 && next < tl.u_total) warm_l2(p, make_unit(p, tl, next), pf, lane);
     int seq = 0, nex = 0;
-    for (int k = 0;; ++k) {
+    for (int k = ld == 0 ? 0 : h_k0 + 1; !idle; k += two ? 2 : 1) {
       if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 1, gtimer());
       const int u_id = __shfl_sync(0xffffffffu, next < tl.u_total ? next : -1, 0);
+      if (kLd2 && ld == 0 && !two && p.mode == MODE_FUSED && u_id >= tl.u1) {
+        // the first expand unit: from here on one stage and one V buffer per unit
+        h_k0 = k;
+        h_seq0 = seq;
+        h_nex0 = nex;
+        if (lane == 0) {
+          sm.ho_k0 = k;
+          sm.ho_seq0 = seq;
+          sm.ho_nex0 = nex;
+          sm.ho_ok = 1;
+          mbar_arrive(&sm.ho_bar);  // release: the handoff values above
+        }
+        two = true;
+      }
+      if (two) {  // this loader's stage and V buffer sequence at position k
+        seq = h_seq0 + (k - h_k0);
+        nex = h_nex0 + (k - h_k0);
+      }
       // publish the unit id to the MMA and epilogue warps
       const int q = k % UQ;
       if (lane == 0) {
         if (k >= UQ) pf_wait(p, &sm.uempty[q], ((k / UQ) - 1) & 1, 3, k, 0);
-        sm.uslot[q] = u_id;
+        sm.uslot[q] = (u_id < 0 && two) ? kUnitLoaderDone : u_id;
         mbar_arrive(&sm.ufull[q]);
         trace_ld(p, k, 0);
       }
@@ -1055,19 +1134,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       }
       if (kWarmL2 && next < tl.u_total) warm_l2(p, make_unit(p, tl, next), pf, lane);
     }
+    if (kLd2 && ld == 0 && !two && lane == 0) {  // no expand units here: loader 1 has nothing to do
+      sm.ho_ok = 0;
+      mbar_arrive(&sm.ho_bar);
+    }
+  } else if (kLd2 && warp == W_PUB) {
+    publisher_both(p, sm);
   } else if (warp == W_PUB || warp == W_PUB + 1) {
     publisher(p, sm, warp - W_PUB);
   } else if (warp == W_MMA) {
     // ---------------------------------------------------------------- MMA issuer
     int seq = 0, nsh = 0, nex = 0, ngrp = 0, ndrain = 0;
+    int skip_par = -1;  // CHAM_PF_LD2: position parity of the loader that finished first
     const uint32_t idesc_ex = idesc_bf16(BM, 64, true);
     for (int k = 0;; ++k) {
       if (k > 0 && lane == 0 && p.trace) trace_put(p, k - 1, 3, gtimer());
+      if (skip_par >= 0 && (k & 1) == skip_par) {  // the finished loader's position: its stage
+        ++seq;                                      // and V buffer advance, nothing else
+        ++nex;
+        continue;
+      }
       const int q = k % UQ;
       pf_wait(p, &sm.ufull[q], (k / UQ) & 1, 7, k, 0);
       const int u_id = sm.uslot[q];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
+      if (u_id == kUnitLoaderDone && skip_par < 0) {
+        ++seq;
+        ++nex;
+        skip_par = k & 1;
+        continue;
+      }
       if (u_id < 0) {
         if (lane == 0) sm.last[1] = ndrain;  // drain phases used (CHAM_PF_MMA_SYNC)
         __syncwarp();
@@ -1167,13 +1264,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     const int r = wq * 32 + lane;  // tile row == TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     int seq = 0, nsh = 0, ngrp = 0, nvb = 0, npost = 0;
+    int skip_par = -1;  // CHAM_PF_LD2: position parity of the loader that finished first
     for (int k = 0;; ++k) {
       if (k > 0 && tid == 0 && p.trace) trace_put(p, k - 1, 5, gtimer());
+      if (skip_par >= 0 && (k & 1) == skip_par) {
+        ++seq;
+        continue;
+      }
       const int q = k % UQ;
       pf_wait(p, &sm.ufull[q], (k / UQ) & 1, 13, k, 0);
       const int u_id = sm.uslot[q];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.uempty[q]);
+      if (u_id == kUnitLoaderDone && skip_par < 0) {
+        ++seq;
+        skip_par = k & 1;
+        continue;
+      }
       if (u_id < 0) {
         post_event(p, sm, es, npost, 0, 0, r);  // the publisher exits
         break;
