@@ -619,6 +619,7 @@ __device__ __forceinline__ bool prologue(const Params& p, Shared& sm) {
 
 __device__ __forceinline__ void abort_launch(const Params& p) {
   pdl_wait();
+  if (threadIdx.x < 32) after_wait(p, 0);  // the next apply's counters are still re-armed
   if (threadIdx.x == 0 && blockIdx.x == 0) *p.err = CHAM_ERR_LIMIT;
 }
 
