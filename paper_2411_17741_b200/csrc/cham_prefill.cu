@@ -50,6 +50,10 @@ constexpr int NS = CHAM_PF_NS;          // ring stages
 #define CHAM_PF_LD2 0  // 1: two loader warps in the expand phase (alternate unit positions; the second publisher warp loads); A/B on C3: 709k vs 763k — the epilogue (y RMW, ~1.7 us per group per set) then limits, and the 64 KiB stages it needs cost 3%
 #endif
 constexpr bool kLd2 = CHAM_PF_LD2 != 0;
+#ifndef CHAM_PF_PUB1
+#define CHAM_PF_PUB1 1  // one publisher warp probes both epilogue sets' queues (test_wait); 0: one warp per set
+#endif
+constexpr bool kPub1 = CHAM_PF_PUB1 != 0;
 #ifndef CHAM_PF_STAGE
 // two big stages: shrink stages carry 2-3 K-chunks (A copies of 2-3 KiB, not 1 KiB); with two
 // loaders every expand unit must fit one stage (4 groups x 16 KiB of B at rank 128)
@@ -1138,10 +1142,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
       sm.ho_ok = 0;
       mbar_arrive(&sm.ho_bar);
     }
-  } else if (kLd2 && warp == W_PUB) {
+  } else if ((kLd2 || kPub1) && warp == W_PUB) {
     publisher_both(p, sm);
-  } else if (warp == W_PUB || warp == W_PUB + 1) {
+  } else if (!kPub1 && (warp == W_PUB || warp == W_PUB + 1)) {
     publisher(p, sm, warp - W_PUB);
+  } else if (warp == W_PUB + 1) {
+    // kPub1 without kLd2: the second publisher warp has no role
   } else if (warp == W_MMA) {
     // ---------------------------------------------------------------- MMA issuer
     int seq = 0, nsh = 0, nex = 0, ngrp = 0, ndrain = 0;
