@@ -518,3 +518,50 @@ def test_tensor_parallel_degree1_uses_fused_apply():
         ref = lora_apply_ref(x, ys[p], perm, seg_off, seg_slot, seg_rank, full[p])
         np.testing.assert_allclose(yd[p].float().cpu().numpy(), ref, rtol=BF16_RTOL, atol=BF16_ATOL)
     pool.close()
+
+
+def test_device_limit_error_leaves_y_and_the_next_apply_intact():
+    """A segment table the host cannot see (device count) that exceeds the pool's token limit:
+    the decode kernel refuses it on the device (error word set, y untouched), and the applies
+    issued after it on the same stream are exact — the refused launch still re-armed the
+    counter set of the apply before it, which the next apply reuses.
+    Ranks 128/64 make more units than CTAs (dynamic claims), and every apply has new inputs,
+    so stale counters would show up as missing or early expand work."""
+    from paper_2411_17741_b200.ops import lora_apply
+
+    rng = np.random.default_rng(11)
+    h = 1024
+    slot_ranks = {0: 128, 1: 64}
+    adapters = make_adapters(rng, slot_ranks, h, h, bf16=True)
+    pool = _pool(1, [h], [h], torch.bfloat16, 24, n_slots=2, max_tokens=64)
+    pool.set_prefill_route(0)  # decode kernel only
+    _install(pool, {s: [adapters[s]] for s in slot_ranks}, slot_ranks)
+    pool.device_error(clear=True)
+    seg_off = [0, 20, 50]
+
+    def checked_apply():
+        x0 = bf16_round(rng.standard_normal((50, h)).astype(np.float32))
+        y0 = bf16_round(rng.standard_normal((50, h)).astype(np.float32))
+        yd = torch.from_numpy(y0).cuda().to(torch.bfloat16)
+        lora_apply(torch.from_numpy(x0).cuda().to(torch.bfloat16), yd, [0, 1], seg_off, [128, 64], pool=pool,
+                   layer=0, proj=0)
+        torch.cuda.synchronize()
+        ref = lora_apply_ref(x0, y0, np.arange(50), np.array(seg_off), np.array([0, 1]), np.array([128, 64]),
+                             adapters)
+        np.testing.assert_allclose(yd.float().cpu().numpy(), bf16_round(ref.astype(np.float32)), rtol=BF16_RTOL,
+                                   atol=BF16_ATOL)
+
+    checked_apply()  # leaves its counter set dirty: the refused launch below must re-arm it
+    x = torch.from_numpy(bf16_round(rng.standard_normal((50, h)).astype(np.float32))).cuda().to(torch.bfloat16)
+    y = torch.from_numpy(bf16_round(rng.standard_normal((50, h)).astype(np.float32))).cuda().to(torch.bfloat16)
+    y_before = y.clone()
+    n_dev = torch.tensor([2], dtype=torch.int32, device="cuda")
+    # 80 tokens in the (device-counted) table of a 64-token pool
+    lora_apply(x, y, [0, 1], [0, 40, 80], [128, 64], pool=pool, layer=0, proj=0, n_seg_dev=n_dev)
+    torch.cuda.synchronize()
+    assert pool.device_error(clear=True) != 0
+    assert torch.equal(y, y_before)
+    for _ in range(3):  # both counter parities after the refused launch
+        checked_apply()
+    assert pool.device_error(clear=True) == 0
+    pool.close()
