@@ -6,10 +6,12 @@
 // least `prefill_min_tokens` tokens (rank <= 128, bf16).
 //
 // ONE persistent, warp-specialised kernel per lora_apply (K3), one CTA per SM, 12
-// warps: 0-7 epilogue (two sets of four, each set covering the 128 TMEM lanes), 8-9 publishers
-// (one per epilogue set), 10 MMA issuer, 11 loader (TMA + dispatch; the highest warp id, so
-// the schedulers favour it).  A tile is up to 128 token rows of one segment (UMMA M = 128).
-// Units come from one dynamic counter, phase-1 units first:
+// warps: 0-7 epilogue (two sets of four, each set covering the 128 TMEM lanes), 8 publisher
+// (probes both sets' queues; warp 9 is the second loader with CHAM_PF_LD2, else idle), 10 MMA
+// issuer, 11 loader (TMA + dispatch; the highest warp id, so the schedulers favour it).  A tile
+// is up to 128 token rows of one segment (UMMA M = 128).  The ring has two 48 KiB stages.
+// Units come from one dynamic counter, phase-1 units first (shrink units in LPT order: tiles
+// by rank, descending; K split <= 2):
 //   shrink unit (tile, K range kq of ks, job group): D[128 x rp] (TMEM, fp32) = X . A^T over the
 //        range, for every job of the group from ONE x stage (q/k/v share x, so x crosses
 //        HBM->SM once per K range).  Stages carry kpc 64-column k-chunks: x by TMA tensor loads
@@ -26,7 +28,9 @@
 //        = V . B per group into one of four TMEM accumulators; the epilogue thread of token
 //        row r loads its 128-byte y piece of the group into registers one group ahead, adds
 //        D2 and stores it back — no separate elementwise kernel, no y in shared memory.
-// Expand units wait only for their own tile, so the phases overlap across tiles.  The path is
+// Expand units wait only for their own tile, so the phases overlap across tiles.  Counters
+// ping-pong by launch parity; each launch re-arms the previous launch's set after its
+// griddepcontrol.wait (no last-CTA reset).  The path is
 // HBM-bound (AI ~15 flop/B at C3): tensor cores are used because the CUDA-core FMA ceiling
 // (~51-74 TFLOP/s) is below what the HBM roofline demands.
 #include <cuda.h>
