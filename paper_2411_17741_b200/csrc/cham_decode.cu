@@ -1,7 +1,7 @@
 // cham_decode.cu — segmented shrink (h_in -> r) and expand (r -> h_out, accumulated into y)
-// for decode-sized segments: ONE persistent, warp-specialised kernel per lora_apply with two
-// phases separated by a grid barrier; consecutive applies overlap through programmatic
-// dependent launch (PDL).
+// for decode-sized segments: ONE persistent, warp-specialised kernel per lora_apply; an
+// expand stage waits only for the shrink units of its own pages (no grid barrier);
+// consecutive applies overlap through programmatic dependent launch (PDL).
 //
 // Reference seam: CostModel.step_duration's LoRA term (engine.py:67-77) models
 //   adapter_units = sum_decoders rank + sum_prefills rank * input_tokens
@@ -15,19 +15,22 @@
 //               bf16 of h_in) + the tile's x rows for that k-chunk; the 8 x T partial sums
 //               stay in registers across the stages, so v is written once, final.
 //      K2 unit = (job, tile, 1024-column chunk): ceil(np/2) stages, each = two pages x
-//               16 KiB of B; the y rows and the tile's v rows ride on the first stage.
-//  * Units are taken dynamically from a global counter (the next index is prefetched while
-//    the current unit streams).  K2 walks segments largest-rank first (LPT), so the tail
-//    is made of the small rank-8 units.
-//  * Warp 8 produces (plan in shared memory: no L2 round trips in the loop), 8 consumer
-//    warps compute with packed FFMA2 (fp32 accumulate).  Weights are issued before
-//    griddepcontrol.wait, activations after it.  Between the phases the producer posts a
-//    marker stage; on it the consumers publish their v rows (release) and arrive at a
-//    sense-reversal grid barrier, while the producer already streams phase-2 B pages and
-//    y rows; only the v copies wait for the barrier (acquire + async-proxy fence).  The
-//    grid is one CTA per SM (co-resident).  Every CTA executes griddepcontrol.wait before
-//    exiting, so apply n completes after apply n-1 and the ping-pong v buffer of apply
-//    n-2 is free when apply n writes it.
+//               16 KiB of B with those pages' v slices; the y rows ride on the last stage
+//               (tiles of <= 4 pages: 2048-column units, one page per stage).
+//  * Units come from ONE global counter, all shrink units then all expand units, each in
+//    LPT order (adapters of larger page count first); two units are fetched ahead of the
+//    one being issued and one more claim is in flight.
+//  * Two producer warps (producer 0 claims and forwards the unit ids, producer 1 issues
+//    every other stage; plan in shared memory), 8 consumer warps (packed FFMA2, fp32
+//    accumulate), one publisher warp: a finished shrink unit's v rows are released with one
+//    `red.release.gpu.or` of its page bit into the tile's mask; an expand stage acquires the
+//    bits of its pages before its v copy.  Weights are issued before griddepcontrol.wait,
+//    activations after it.
+//  * Counters and the fp32 v workspace ping-pong by apply parity.  Producer 0 of every CTA
+//    re-arms the previous apply's counter slice right after griddepcontrol.wait and only then
+//    signals launch_dependents, so apply n+1 starts with zeroed counters and no CTA ends with
+//    a last-CTA reset; every CTA executes griddepcontrol.wait, so apply n completes after
+//    apply n-1 and the v buffer of apply n-2 is free when apply n writes it.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
