@@ -25,7 +25,7 @@
 //   expand unit (tile, job, CW = 256 columns): the loader waits for the tile's images, copies
 //        the V image (one bulk copy, double-buffered), then streams the B page slices of the
 //        unit's 64-column groups (MN-major SWIZZLE_128B — the pool layout again).  D2[128 x 64]
-//        = V . B per group into one of four TMEM accumulators; the epilogue thread of token
+//        = V . B per group into one of two TMEM accumulators; the epilogue thread of token
 //        row r loads its 128-byte y piece of the group into registers one group ahead, adds
 //        D2 and stores it back — no separate elementwise kernel, no y in shared memory.
 // Expand units wait only for their own tile, so the phases overlap across tiles.  Counters
@@ -115,10 +115,16 @@ constexpr int kUnitLoaderDone = -2;  // kLd2: a loader ran out of units (its lat
 constexpr int PQN = 8;                  // publish ring depth per epilogue set
 constexpr int TMEM_COLS = 512;
 // TMEM: two shrink accumulators of TM_SH columns, then NACC expand accumulators of 64 columns
-// (register-y path: 2 x 128 + 4 x 64, so four expand groups are in flight between the MMA
-// warp and the epilogue; staged-y path: 2 x 192 + 2 x 64)
-constexpr int NACC = CHAM_PF_YREG ? 4 : 2;
-constexpr int TM_SH = CHAM_PF_YREG ? 128 : 192;
+// (2 x 128 + 2 x 64: one expand group per epilogue set in flight between the MMA warp and
+// the epilogue; four measured 0.6% slower)
+#ifndef CHAM_PF_NACC
+#define CHAM_PF_NACC 2  // expand accumulators; A/B on C3 (register y path): 2 -> 762k, 4 -> 757k, 6 (TM_SH 64) -> 743k
+#endif
+#ifndef CHAM_PF_TMSH
+#define CHAM_PF_TMSH (CHAM_PF_YREG ? 128 : 192)
+#endif
+constexpr int NACC = CHAM_PF_NACC;
+constexpr int TM_SH = CHAM_PF_TMSH;
 constexpr int TM_EX = 2 * TM_SH;
 static_assert(TM_EX + NACC * 64 <= TMEM_COLS, "TMEM budget");
 constexpr int BAR_EPI = 1;              // named barriers 1, 2: the 128 threads of epilogue set 0, 1
