@@ -82,7 +82,10 @@ constexpr bool kYPrefetch = CHAM_PF_YPF != 0;
 #endif
 constexpr int CW = CHAM_PF_CW;          // expand unit columns
 constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
-constexpr int UQ = 8;                   // unit-id ring depth
+#ifndef CHAM_PF_UQ
+#define CHAM_PF_UQ 8
+#endif
+constexpr int UQ = CHAM_PF_UQ;          // unit-id ring depth
 #ifndef CHAM_PF_ZERO_NEXT
 #define CHAM_PF_ZERO_NEXT 1  // counters re-armed by the next launch after its griddepcontrol.wait
 #endif
