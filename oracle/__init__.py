@@ -6,12 +6,13 @@ legs may use it, and only as the checker or the timed CPU baseline, never as the
 measured or shipped.
 
 Contents and pinning status:
-  * lora_ref.py     — numpy restatement of y += (x . A_i) . B_i per segment.  PARITY
-                      UNPINNED by the reference: the reference (adaptersim) only models this
-                      as a cost term (engine.py:67-77); the paper's arithmetic lived in the
-                      third-party S-LoRA kernels, which are not vendored.  The restatement
-                      follows the north-star definition and is checked for self-consistency
+  * lora_ref.py     — numpy restatement of y += (x . A_i) . B_i per segment.  The reference
+                      (adaptersim) only models this as a cost term (engine.py:67-77); the
+                      paper's arithmetic lived in the un-vendored third-party S-LoRA kernels.
+                      Pinned to third-party golden vectors (vLLM 0.22.0 Punica SGMV torch ops,
+                      punica_golden.py -> tests/golden/punica_sgmv.npz) and self-checked
                       (linearity, rank-padding, fp64 agreement) in tests/test_oracle.py.
+  * punica_golden.py — generates those vectors (run in this container, where vLLM imports).
   * segments_ref.py — numpy restatement of the segment-table builder; pinned against the
                       reference engine's own batch arithmetic (sum of rank * tokens per step,
                       engine.py:64-77) on batches captured from the reference simulate().

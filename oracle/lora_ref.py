@@ -7,8 +7,11 @@ model.py:23-26: two matrices per projection).  Token -> rank attribution follows
 reference cost model: a decoder contributes 1 token, a prefill `input_tokens` tokens
 (engine.py:64-76).
 
-PARITY UNPINNED: the reference never computes this product (SPEC.md:12 puts GPU kernels out
-of scope; PAPER.md:139-141 delegates them to third-party S-LoRA, not vendored).
+The reference never computes this product (SPEC.md:12 puts GPU kernels out of scope;
+PAPER.md:139-141 delegates them to third-party S-LoRA, not vendored).  This restatement is
+pinned instead to third-party golden vectors: vLLM 0.22.0's torch Punica SGMV shrink/expand
+(the published algorithm S-LoRA implements), tests/golden/punica_sgmv.npz made by
+oracle/punica_golden.py and checked in tests/test_punica_golden.py.
 """
 from __future__ import annotations
 
