@@ -3,9 +3,10 @@
 // Replaces the per-request Python loop of CostModel.step_duration (engine.py:64-76), which
 // walks the step's batch (prefills with input_tokens each, decoders with one token each,
 // engine.py:443-451) one request at a time.  Here one CTA of 1024 threads builds the
-// stable group-by-slot of up to 4096 requests with a block radix sort (CUB, stable), block
-// scans for token offsets and segment ids, and writes perm / seg_off / seg_slot / seg_rank.
-// Slots must be < 2^20.  Canonical form (bit-exact with oracle/segments_ref.py): segments in ascending slot order,
+// stable group-by-slot of up to 4096 requests with a block radix sort (CUB, stable) over
+// only the bits the batch's largest slot needs (7 bits = 2 digit passes for 100 adapters,
+// instead of 8 passes over slot << 12 | request), block scans for token offsets and segment
+// ids, and writes perm / seg_off / seg_slot / seg_rank.  Slots must be < 2^20.  Canonical form (bit-exact with oracle/segments_ref.py): segments in ascending slot order,
 // requests inside a segment in batch order, tokens of a request contiguous.
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
@@ -32,6 +33,7 @@ build_segments_kernel(const int* __restrict__ req_slot, const int* __restrict__ 
   } tmp;
   __shared__ unsigned last_key[kThreads];
   __shared__ int total_tokens, total_segs;
+  __shared__ unsigned s_max_slot;
 
   const int tid = threadIdx.x;
   // 1) token offsets in batch order (blocked arrangement: thread t owns requests 4t..4t+3)
@@ -42,34 +44,49 @@ build_segments_kernel(const int* __restrict__ req_slot, const int* __restrict__ 
     ntok[i] = r < n_req ? max(req_ntok[r], 0) : 0;
   }
   int off[kItems];
+  if (tid == 0) s_max_slot = 0;
   Scan(tmp.scan).ExclusiveSum(ntok, off);
-  __syncthreads();
-
-  // 2) sort of key = slot << 12 | request index (unique keys, so batch order is kept inside
-  //    a slot); the value carries the request's first token.  No adapter -> sorts last.
-  unsigned key[kItems];
-  int val[kItems];
+  int slot_in[kItems];
+  unsigned my_max = 0;
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
     const int r = tid * kItems + i;
     const int s = r < n_req ? req_slot[r] : -1;
-    key[i] = (s >= 0 && s < (1 << 20)) ? ((static_cast<unsigned>(s) << 12) | r) : 0xffffffffu;
-    val[i] = off[i];
+    slot_in[i] = (s >= 0 && s < (1 << 20)) ? s : -1;
+    if (slot_in[i] >= 0) my_max = max(my_max, static_cast<unsigned>(slot_in[i]) + 1);
   }
-  Sort(tmp.sort).Sort(key, val);
+  __syncthreads();
+  if (my_max) atomicMax(&s_max_slot, my_max);
+  __syncthreads();
+
+  // 2) stable sort of key = slot (batch order kept inside a slot: CUB's radix sort is
+  //    stable and the input is in batch order); the value is the request index.  No adapter
+  //    -> key = largest slot + 1, sorts last.  Only the bits of that sentinel are sorted.
+  //    The value packs the request's first token (< 2^20: a step holds at most 65535 tokens,
+  //    kMaxPoolTokens) above its 12-bit index.
+  const unsigned sentinel = s_max_slot;  // largest valid slot + 1
+  const int end_bit = max(1, 32 - __clz(sentinel));
+  unsigned key[kItems];
+  int val[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    key[i] = slot_in[i] >= 0 ? static_cast<unsigned>(slot_in[i]) : sentinel;
+    val[i] = (off[i] << 12) | (tid * kItems + i);
+  }
+  Sort(tmp.sort).Sort(key, val, 0, end_bit);
   __syncthreads();
 
   // 3) token positions in grouped order and segment ids
   int gtok[kItems], flag[kItems];
   last_key[tid] = key[kItems - 1];
   __syncthreads();
-  unsigned prev = tid > 0 ? (last_key[tid - 1] >> 12) : 0xfffffffeu;
+  unsigned prev = tid > 0 ? last_key[tid - 1] : 0xfffffffeu;
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
-    const bool valid = key[i] != 0xffffffffu;
-    gtok[i] = valid ? max(req_ntok[key[i] & 4095], 0) : 0;
-    flag[i] = valid && (key[i] >> 12) != prev ? 1 : 0;
-    prev = key[i] >> 12;
+    const bool valid = key[i] != sentinel;
+    gtok[i] = valid ? max(req_ntok[val[i] & 4095], 0) : 0;
+    flag[i] = valid && key[i] != prev ? 1 : 0;
+    prev = key[i];
   }
   int gpos[kItems], segid[kItems];
   int tot_tok, tot_seg;
@@ -82,14 +99,14 @@ build_segments_kernel(const int* __restrict__ req_slot, const int* __restrict__ 
   }
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
-    if (key[i] == 0xffffffffu) continue;
-    const int r = key[i] & 4095;
+    if (key[i] == sentinel) continue;
+    const int r = val[i] & 4095;
     if (flag[i]) {
       seg_off[segid[i]] = gpos[i];
-      seg_slot[segid[i]] = static_cast<int>(key[i] >> 12);
+      seg_slot[segid[i]] = static_cast<int>(key[i]);
       seg_rank[segid[i]] = req_rank[r];
     }
-    const int base = val[i];
+    const int base = static_cast<unsigned>(val[i]) >> 12;
     for (int k = 0; k < gtok[i]; ++k) perm[gpos[i] + k] = base + k;
   }
   __syncthreads();

@@ -186,10 +186,13 @@ def test_device_segment_builder_bit_exact():
     from paper_2411_17741_b200.ops import build_segments
 
     rng = np.random.default_rng(7)
-    for n_req, n_slots in [(1, 1), (256, 82), (4096, 1000), (333, 7), (64, 64)]:
+    # (requests, slots, most tokens per request): the sort covers only the bits of the
+    # largest slot + 1, so cover no-adapter-only batches, one slot, and slots near 2^20
+    for n_req, n_slots, mt in [(1, 1, 6), (256, 82, 6), (4096, 1000, 6), (333, 7, 6), (64, 64, 6), (50, 0, 6),
+                               (300, 1 << 20, 200), (4096, 2, 16), (17, 255, 3), (600, 256, 3)]:
         slots = rng.integers(-1, n_slots, n_req)
         ranks = rng.choice([8, 16, 32, 64, 128], n_req)
-        ntok = rng.integers(1, 6, n_req)
+        ntok = rng.integers(1, mt, n_req)
         tbl = build_segments(slots, ranks, ntok)
         torch.cuda.synchronize()
         got = tbl.to_host()
