@@ -413,6 +413,8 @@ struct TileList {
   int ks;           // shrink K-split factor
   int u1;           // phase-1 units
   int u_total;
+  int ncc, ept;     // expand: column chunks per (tile, job); units per tile (n_jobs x ncc)
+  float inv_ncc, inv_ept;  // their reciprocals (fast division on the loader's path)
   int sh_start[MAX_TILES + 1];  // phase-1 unit prefix over the LPT order
   int ord[MAX_TILES];            // LPT order of the phase-1 units: position -> tile (rank descending)
   Tile t[MAX_TILES];
@@ -520,8 +522,21 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
     tl.u1 = carry;
     const int ncc = (p.h_out + CW - 1) / CW;
     tl.u_total = carry + ((p.mode == MODE_SHRINK || p.no_expand) ? 0 : tiles * p.n_jobs * ncc);
+    tl.ncc = ncc;
+    tl.ept = p.n_jobs * ncc;
+    tl.inv_ncc = 1.0f / (float)ncc;
+    tl.inv_ept = 1.0f / (float)tl.ept;
   }
   return true;
+}
+
+// n / d for 0 <= n < 2^24 by the reciprocal (one correction step: the float quotient is off
+// by at most one); replaces the ~30-instruction integer division on the loader's per-unit path
+__device__ __forceinline__ int fdiv(int n, int d, float inv) {
+  int q = __float2int_rz(__int2float_rn(n) * inv);
+  const int r = n - q * d;
+  q += r >= d ? 1 : r < 0 ? -1 : 0;
+  return q;
 }
 
 __device__ __forceinline__ int tile_of_unit(const TileList& tl, int u) {
@@ -556,11 +571,11 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
     x.tile = tl.ord[k];
     x.kind = p.mode == MODE_EXPAND ? 3 : 1;
   } else {
-    const int ncc = (p.h_out + CW - 1) / CW;
+    const int ncc = tl.ncc;
     const int r = u - tl.u1;
-    x.tile = r / (p.n_jobs * ncc);
-    const int jc = r - x.tile * p.n_jobs * ncc;
-    x.job = jc / ncc;
+    x.tile = fdiv(r, tl.ept, tl.inv_ept);
+    const int jc = r - x.tile * tl.ept;
+    x.job = fdiv(jc, ncc, tl.inv_ncc);
     x.col0 = (jc - x.job * ncc) * CW;
     x.kind = 2;
   }
@@ -578,10 +593,11 @@ __device__ __forceinline__ Unit make_unit(const Params& p, const TileList& tl, i
   x.vstride = ((x.rp + 63) / 64) * x.xb;
   if (x.kind == 1) {
     const int rem = u - tl.sh_start[k];
-    x.kq = rem % t.ks;
+    const int lks = __ffs(t.ks) - 1;  // ks is a power of two
+    x.kq = rem & (t.ks - 1);
     x.jps = jobs_per_group(p, t.rank);
-    x.job0 = (rem / t.ks) * x.jps;
-    x.nchunks = (p.h_in / 64) / t.ks;
+    x.job0 = (rem >> lks) * x.jps;
+    x.nchunks = (p.h_in / 64) >> lks;
     const int chunk_bytes = x.xb + x.jps * (x.rp / 8) * kAtomBytes;
     x.kpc = max(1, min(4, min(STAGE / chunk_bytes, x.nchunks)));
     x.nst = (x.nchunks + x.kpc - 1) / x.kpc;
@@ -616,7 +632,7 @@ __device__ __forceinline__ Prefetch prefetch_unit(const Params& p, const TileLis
   }
   const bool ok = u_id >= 0 && u_id < tl.u_total;
   const int uu = ok ? u_id : 0;
-  const int ti = uu < tl.u1 ? tl.ord[tile_of_unit(tl, uu)] : (uu - tl.u1) / (p.n_jobs * ((p.h_out + CW - 1) / CW));
+  const int ti = uu < tl.u1 ? tl.ord[tile_of_unit(tl, uu)] : fdiv(uu - tl.u1, tl.ept, tl.inv_ept);
   const Tile& t = tl.t[ti];
   f.page = __ldg(p.slot_pages + t.slot * kMaxPagesPerSlot + min(lane, kMaxPagesPerSlot - 1));
 #pragma unroll
@@ -924,10 +940,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
     }
     if (dyn && lane < CD && next < tl.u_total) claim = atomicAdd(p.ctr, 1);
     // published phase-1 units of an expand unit's tile, read without blocking one unit ahead
-    const int ex_per_tile = p.n_jobs * ((p.h_out + CW - 1) / CW);
     auto peek_flag = [&](int u) {  // unconditional (clamped) load: the value is used one unit later
       int v;
-      const int* f = p.tile_cnt + min(max(u - tl.u1, 0) / ex_per_tile, MAX_TILES - 1);
+      const int* f = p.tile_cnt + min(fdiv(max(u - tl.u1, 0), tl.ept, tl.inv_ept), MAX_TILES - 1);
       asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       return v;
     };
