@@ -86,6 +86,10 @@ constexpr int NGRP = CW / 64;           // 64-column MMA groups per expand unit
 #define CHAM_PF_UQ 8
 #endif
 constexpr int UQ = CHAM_PF_UQ;          // unit-id ring depth
+#ifndef CHAM_PF_ZATOM
+#define CHAM_PF_ZATOM 1  // odd page counts read their K padding from one zero atom (the last K step's stride points at it); 0: the loader zero-fills a pad atom per stage (A/B on C3: 775.9k vs 774.0k tok/s)
+#endif
+constexpr bool kZeroAtom = CHAM_PF_ZATOM != 0;
 #ifndef CHAM_PF_ZERO_NEXT
 #define CHAM_PF_ZERO_NEXT 1  // counters re-armed by the next launch after its griddepcontrol.wait
 #endif
@@ -427,7 +431,8 @@ __device__ __forceinline__ int jobs_per_group(const Params& p, int rank) {
   return (p.mode == MODE_FUSED && p.x_shared && p.n_jobs * (rpad(rank) / 8) <= 16 && p.n_jobs * rpad(rank) <= TM_SH)
              ? p.n_jobs : 1;
 }
-__device__ __forceinline__ int n_groups(const Params& p, int rank) { return p.n_jobs / jobs_per_group(p, rank); }
+// job groups of a tile (jobs_per_group is n_jobs or 1): no integer division on the loader's path
+__device__ __forceinline__ int n_groups(const Params& p, int rank) { return jobs_per_group(p, rank) == 1 ? p.n_jobs : 1; }
 
 // Warp 0 of every CTA builds the same tile list (deterministic): prefill segments in table
 // order, each cut into 128-row tiles; phase-1 unit prefix per tile.  Returns false on overflow.
@@ -717,6 +722,7 @@ struct Shared {
   // read (and ignored) from whatever follows it.  Each V buffer has its own pad so that read
   // never overlaps the other buffer, which the loader may be filling (TMA) at the same time.
   alignas(1024) unsigned char vbuf[2][VBUF + VPAD];
+  alignas(1024) unsigned char zero_atom[kZeroAtom ? kAtomBytes : 16];  // above every ring stage
   uint64_t full[NS], empty[NS];
   uint64_t tfull_sh[2], tempty_sh[2], tfull_ex[NACC], tempty_ex[NACC];
   uint64_t vfull[2], vempty[2];
@@ -868,6 +874,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
         mbar_init(&sm.pq_empty[e][i], 1);
       }
     fence_mbar_init();
+  }
+  if (kZeroAtom && warp == W_MMA) {  // zeros for the MMA's async-proxy reads (before the CTA barrier below)
+    for (int i = lane; i < kAtomBytes / 16; i += 32) reinterpret_cast<uint4*>(sm.zero_atom)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_shared();
   }
   if (!CHAM_PF_NOPFMAP && warp == W_LOAD && lane < p.n_jobs) {
     prefetch_map(&p.maps[lane].x64);
@@ -1111,7 +1121,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
           c64[0] = block64(contig, rows, nblk, 0);
           c64[1] = nblk > 2 && block64(contig, rows, nblk, 1);
         }
-        const bool pad = (u.rp / 8) > u.np;
+        const bool pad = !kZeroAtom && (u.rp / 8) > u.np;
         for (int s = 0; s < u.nst; ++s, ++seq) {
           const int st = seq % NS;
           const int g_first = s * u.kpc;
@@ -1270,9 +1280,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_kernel(const __grid_constan
             if (lane == 0) {
               const uint32_t ba = base + g * kAtomBytes;  // B atoms [page][group]
               // D2 = V . B over the tile's (reduced) V image
-              for (int kk = 0; kk < u.rp / 16; ++kk) {
+              const int nk = u.rp / 16;
+              const bool zpad = kZeroAtom && 2 * nk > u.np;  // odd page count: K rows rank..rp
+              for (int kk = 0; kk < nk; ++kk) {
                 const uint64_t ad = sdesc(va + (kk >> 2) * u.xb + (kk & 3) * 32, 16, 1024);
-                const uint64_t bd = sdesc(ba + kk * 2 * u.kpc * kAtomBytes, kAtomBytes, u.kpc * kAtomBytes);
+                const uint32_t b0 = ba + kk * 2 * u.kpc * kAtomBytes;
+                // the second 8-row K group of the last step comes from the zero atom
+                const uint32_t ks = (zpad && kk == nk - 1) ? smem_u32(sm.zero_atom) - b0 : u.kpc * kAtomBytes;
+                const uint64_t bd = sdesc(b0, kAtomBytes, ks);
                 mma_bf16(tmem + TM_EX + acc * 64, ad, bd, idesc_ex, kk ? 1u : 0u);
               }
               mma_commit(&sm.tfull_ex[acc]);
