@@ -535,8 +535,10 @@ __device__ bool build_tiles(const Params& p, TileList& tl, int grid) {
   return true;
 }
 
-// n / d for 0 <= n < 2^24 by the reciprocal (one correction step: the float quotient is off
-// by at most one); replaces the ~30-instruction integer division on the loader's per-unit path
+// n / d for 0 <= n < 2^22 by the reciprocal (one correction step: the float quotient is off
+// by at most one there); replaces the ~30-instruction integer division on the loader's
+// per-unit path.  Unit counts stay far below 2^22; the tile peek of an exhausted claim
+// (n ~ 2^29) gets a quotient within a few units of the true one, which the caller clamps.
 __device__ __forceinline__ int fdiv(int n, int d, float inv) {
   int q = __float2int_rz(__int2float_rn(n) * inv);
   const int r = n - q * d;
